@@ -1,0 +1,124 @@
+#include "cube.hpp"
+
+#include <cstdint>
+
+namespace c3d {
+
+size_t dtype_size(int dtype) { return dtype == kF32 ? 4 : 2; }
+
+namespace {
+
+ncclDataType_t nccl_type(int dtype) { return dtype == kF32 ? ncclFloat32 : ncclBfloat16; }
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    fail(C3D_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+}  // namespace
+
+Cube::Cube(const int dims[3], int rank, int device, const unsigned char* uid)
+    : grid_(dims), rank_(rank), device_(device) {
+  coords_ = grid_.coords_of(rank);
+  C3D_CUDA(cudaSetDevice(device));
+  C3D_CUDA(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device));
+  // Keep pooled scratch resident: collectives and kernels reuse it every step.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  if (grid_.size() > 1) {
+    if (uid == nullptr) fail(C3D_ERR_CONFIG_INVALID, "multi-rank grid needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    nccl_check(ncclCommInitRank(&world_, grid_.size(), id, rank), "ncclCommInitRank");
+    for (int a = 0; a < 3; ++a) {
+      if (grid_.dims[a] == 1) continue;  // uniform across ranks: all skip together
+      const int color = grid_.line_index(coords_, a);
+      nccl_check(ncclCommSplit(world_, color, coords_[a], &axis_comm_[a], nullptr),
+                 "ncclCommSplit");
+    }
+  }
+}
+
+Cube::~Cube() {
+  for (auto& c : axis_comm_)
+    if (c) ncclCommDestroy(c);
+  if (world_) ncclCommDestroy(world_);
+}
+
+ncclComm_t Cube::comm(int axis) const {
+  if (axis < 0 || axis > 2 || !axis_comm_[axis])
+    fail(C3D_ERR_INTERNAL, "no communicator for axis " + std::to_string(axis));
+  return axis_comm_[axis];
+}
+
+void Cube::charge(int kind, uint64_t sent, uint64_t received) {
+  counters_.elements_sent += sent;
+  counters_.elements_received += received;
+  counters_.sent_by_kind[kind] += sent;
+  counters_.received_by_kind[kind] += received;
+  counters_.calls_by_kind[kind] += 1;
+}
+
+void Cube::all_gather(int axis, const void* send, void* recv, size_t count, int dtype,
+                      cudaStream_t s) {
+  const int p = extent(axis);
+  if (p == 1) {
+    if (send != recv)
+      C3D_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dtype), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  nccl_check(ncclAllGather(send, recv, count, nccl_type(dtype), comm(axis), s), "ncclAllGather");
+  charge(C3D_ALL_GATHER, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
+}
+
+void Cube::reduce_scatter(int axis, const void* send, void* recv, size_t count, int dtype,
+                          cudaStream_t s) {
+  const int p = extent(axis);
+  if (p == 1) {
+    if (send != recv)
+      C3D_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dtype), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  nccl_check(ncclReduceScatter(send, recv, count, nccl_type(dtype), ncclSum, comm(axis), s),
+             "ncclReduceScatter");
+  charge(C3D_REDUCE_SCATTER, static_cast<uint64_t>(p - 1) * count,
+         static_cast<uint64_t>(p - 1) * count);
+}
+
+void Cube::all_reduce(int axis, void* buf, size_t count, int dtype, bool is_max, cudaStream_t s) {
+  const int p = extent(axis);
+  if (p == 1) return;
+  nccl_check(ncclAllReduce(buf, buf, count, nccl_type(dtype), is_max ? ncclMax : ncclSum,
+                           comm(axis), s),
+             "ncclAllReduce");
+  charge(C3D_ALL_REDUCE, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
+}
+
+void Cube::broadcast(int axis, int root_position, void* buf, size_t count, int dtype,
+                     cudaStream_t s) {
+  const int p = extent(axis);
+  if (root_position < 0 || root_position >= p)
+    fail(C3D_ERR_OUT_OF_RANGE, "broadcast root position " + std::to_string(root_position));
+  if (p == 1) return;
+  nccl_check(ncclBroadcast(buf, buf, count, nccl_type(dtype), root_position, comm(axis), s),
+             "ncclBroadcast");
+  if (coords_[axis] == root_position)
+    charge(C3D_BROADCAST, static_cast<uint64_t>(p - 1) * count, 0);
+  else
+    charge(C3D_BROADCAST, 0, count);
+}
+
+void Cube::barrier(cudaStream_t s) {
+  if (grid_.size() == 1) return;
+  // A zero-payload all-reduce over the world communicator orders all ranks.
+  DevBuf one(sizeof(float), s);
+  C3D_CUDA(cudaMemsetAsync(one.get(), 0, sizeof(float), s));
+  nccl_check(ncclAllReduce(one.get(), one.get(), 1, ncclFloat32, ncclSum, world_, s),
+             "ncclAllReduce(barrier)");
+  counters_.calls_by_kind[C3D_BARRIER] += 1;
+}
+
+}  // namespace c3d

@@ -1,0 +1,72 @@
+// HBM-bound row / column / elementwise kernels of the layer path. Each cites the
+// reference loop it replaces.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gemm.hpp"
+
+namespace c3d {
+
+// Generic elementwise epilogue over a contiguous rows x cols matrix `in`
+// (same semantics as the GEMM epilogue with acc = in[m][n]); e.out may alias in.
+// Covers add_vec_fwd (cube3d/ops3d.hpp:352-356), GELU (cube3d/transformer.hpp:51),
+// GELU' (cube3d/transformer.hpp:60-61) and the residual add_into (:105-111).
+void k_apply_epilogue(const void* in, int in_dtype, int64_t rows, int64_t cols,
+                      const Epilogue& e, cudaStream_t s);
+
+// out[c] = sum_r x[r][c] (* y[r][c] if y), fp32, deterministic order.
+// add_vec_bwd colsum (cube3d/ops3d.hpp:365-367), mul_vec_bwd (:408-413), LN dbeta/dgamma.
+void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int64_t cols,
+              float* out, cudaStream_t s);
+
+void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
+
+// c[r][col] = a[r][col] * b[col] (mul_vec_fwd, cube3d/ops3d.hpp:391-393).
+void k_mul_cols(const void* a, int adt, const float* b, void* c, int cdt, int64_t rows,
+                int64_t cols, cudaStream_t s);
+
+// ---- LayerNorm (cube3d/nn.hpp:140-222) ----
+// out[r] = sum_c x[r][c]               (mean == nullptr)
+// out[r] = sum_c (x[r][c] - mean[r])^2 (mean given; `sum_is_total`: mean = out_sum*inv_h)
+void k_row_sum(const void* x, int dt, int64_t rows, int64_t cols, const float* sums,
+               float inv_h, float* out, cudaStream_t s);
+// y = gamma * xhat + beta with xhat = (x - sum*inv_h) * rsqrt(sq*inv_h + eps).
+void k_ln_apply(const void* x, int dt, int64_t rows, int64_t cols, const float* sums,
+                const float* sq, float inv_h, float eps, const float* gamma, const float* beta,
+                void* y, int ydt, void* xhat, int xhdt, float* inv_std, cudaStream_t s);
+// Single-kernel forward when the hidden dimension is not partitioned.
+void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps,
+                    const float* gamma, const float* beta, void* y, int ydt, void* xhat,
+                    int xhdt, float* inv_std, cudaStream_t s);
+// row_sum[r] = sum_c dy*gamma, row_dot[r] = sum_c dy*gamma*xhat (into rs[0:rows], rs[rows:2rows]).
+void k_ln_bwd_rows(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                   int64_t rows, int64_t cols, float* rs, cudaStream_t s);
+// dx = inv_std*(dy*gamma - row_sum*inv_h - xhat*row_dot*inv_h) (+ resid).
+void k_ln_bwd_dx(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                 const float* inv_std, const float* rs, float inv_h, int64_t rows, int64_t cols,
+                 const void* resid, int rdt, void* dx, int dxdt, cudaStream_t s);
+
+// ---- attention softmax (cube3d/attention.hpp:106-126, 161-169) ----
+void k_softmax_rowmax(const void* sc, int dt, int64_t rows, int64_t cols, float* mx,
+                      cudaStream_t s);
+void k_softmax_rowexpsum(const void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
+                         float* sum, cudaStream_t s);
+void k_softmax_norm(void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
+                    const float* sum, cudaStream_t s);
+void k_softmax_fused(void* sc, int dt, int64_t rows, int64_t cols, cudaStream_t s);
+void k_softmax_bwd_rowdot(const void* dp, const void* p, int dt, int64_t rows, int64_t cols,
+                          float* rowdot, cudaStream_t s);
+void k_softmax_bwd_ds(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
+                      const float* rowdot, float scale, cudaStream_t s);
+void k_softmax_bwd_fused(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
+                         float scale, cudaStream_t s);
+
+// dst[r][h*dst_hs + t] = src[r][h*src_hs + t], t < dh (head-major column blocks).
+void k_copy_heads(const void* src, int64_t src_ld, int64_t src_hs, void* dst, int64_t dst_ld,
+                  int64_t dst_hs, int64_t rows, int64_t heads, int64_t dh, int dt,
+                  cudaStream_t s);
+
+}  // namespace c3d

@@ -1,0 +1,519 @@
+// 3-D Linear, LayerNorm, attention, MLP and Transformer layer, forward and
+// backward, per rank. Orchestration mirrors the reference call stacks
+// (SURVEY.md §3 (2)/(3)); the per-slice attention loop of the reference
+// (cube3d/attention.hpp:96-133, 128 iterations and 4 collectives each at
+// config 3) becomes batched GEMMs over all local (batch, head) slices with one
+// collective per step, and residual adds / bias / GELU / GELU' are fused into
+// GEMM epilogues whenever no reduce-scatter intervenes.
+#include <cmath>
+#include <string>
+
+#include "common.hpp"
+#include "kernels.hpp"
+#include "nn.hpp"
+
+namespace c3d {
+
+namespace {
+
+View mk_view(const void* base, int dtype, int64_t sr, int64_t sc) {
+  View v;
+  v.base = const_cast<void*>(base);
+  v.dtype = dtype;
+  v.sr = sr;
+  v.sc = sc;
+  return v;
+}
+
+const void* offset(const void* p, int64_t elems, int dtype) {
+  return static_cast<const char*>(p) + elems * static_cast<int64_t>(dtype_size(dtype));
+}
+
+}  // namespace
+
+Act make_act(const Cube& cube, void* data, int dtype, int64_t batch, int64_t seq, int64_t hidden,
+             int group) {
+  const ActGeom g = act_geom(cube.grid(), batch, seq, hidden, group);
+  Act a;
+  a.data = data;
+  a.dtype = dtype;
+  a.batch = batch;
+  a.seq = seq;
+  a.hidden = hidden;
+  a.group = group;
+  a.rows = g.bl * g.sl;
+  a.cols = g.hl;
+  return a;
+}
+
+// flatten (cube3d/activation.hpp:67-79): the activation's Input-layout matrix view.
+Mat flatten(const Cube& cube, const Act& a) {
+  return make_mat(cube, a.data, a.dtype, a.batch * a.seq, a.hidden, kInput,
+                  triple_for_group(a.group));
+}
+
+void validate_config(const Cube& cube, const Config& cfg) {
+  // TransformerConfig::validate (cube3d/nn.hpp:29-40), per-axis extents.
+  const Grid& g = cube.grid();
+  if (cfg.batch <= 0 || cfg.seq <= 0 || cfg.heads <= 0 || cfg.hidden <= 0)
+    fail(C3D_ERR_CONFIG_INVALID, "batch, seq, heads and hidden must be positive");
+  if (g.dims[1] != g.dims[2])
+    fail(C3D_ERR_CONFIG_INVALID, "layer ops need py == pz (got " + std::to_string(g.dims[1]) +
+                                     " and " + std::to_string(g.dims[2]) + ")");
+  const int64_t q = g.dims[1], r = g.dims[0];
+  if (cfg.batch % r) fail(C3D_ERR_CONFIG_INVALID, "batch must be divisible by px");
+  if (cfg.seq % q) fail(C3D_ERR_CONFIG_INVALID, "seq must be divisible by p");
+  const int64_t p2 = g.cubic() ? q * q : q * r;
+  if (cfg.hidden % p2) fail(C3D_ERR_CONFIG_INVALID, "hidden must be divisible by p^2");
+  if ((4 * cfg.hidden) % p2) fail(C3D_ERR_CONFIG_INVALID, "4*hidden must be divisible by p^2");
+  if (cfg.heads % q)
+    fail(C3D_ERR_HEADS_INDIVISIBLE,
+         "heads=" + std::to_string(cfg.heads) + " not divisible by p=" + std::to_string(q));
+  if (cfg.hidden % cfg.heads) fail(C3D_ERR_CONFIG_INVALID, "hidden must be divisible by heads");
+}
+
+// ------------------------------------------------------------------ Linear
+
+void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group, Act& y,
+                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s) {
+  // linear3d_fwd (cube3d/nn.hpp:81-97)
+  if (x.group != group)
+    fail(C3D_ERR_GROUP_MISMATCH, "activation group " + std::to_string(x.group) +
+                                     " does not match state " + std::to_string(group));
+  if (p.input_group != x.group)
+    fail(C3D_ERR_GROUP_MISMATCH, "layer parameters were partitioned for input group " +
+                                     std::to_string(p.input_group));
+  Mat xf = flatten(cube, x);
+  if (p.w.layout != kWeight) fail(C3D_ERR_SHAPE_MISMATCH, "B of C=AB must be Weight layout");
+  if (xf.dirs != p.w.dirs)
+    fail(C3D_ERR_DIRECTION_CLASH, "A and B of C=AB must share one direction triple");
+  if (xf.gcols != p.w.grows)
+    fail(C3D_ERR_SHAPE_MISMATCH, "C=AB needs A cols == B rows, got " +
+                                     std::to_string(xf.gcols) + " vs " + std::to_string(p.w.grows));
+  if (p.b.len != p.w.gcols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "vector length " + std::to_string(p.b.len) +
+                                     " does not match matrix cols " + std::to_string(p.w.gcols));
+  DevBuf bias = expand_diagonal(cube, xf.dirs.swapped(), p.b, s);
+  Mat c;
+  c.data = y.data;
+  c.dtype = y.dtype;
+  LinearEpi e = extra;
+  e.bias = bias.as<float>();
+  ab_forward(cube, mode, xf, p.w, c, e, s);
+  group = 1 - group;
+  y = make_act(cube, y.data, y.dtype, x.batch, x.seq, p.w.gcols, group);
+  if (saved) {
+    saved->x = xf;
+    if (own_input) {
+      DevBuf& cp = saved->keep(DevBuf(xf.elems() * dtype_size(xf.dtype), s));
+      C3D_CUDA(cudaMemcpyAsync(cp.get(), xf.data, xf.elems() * dtype_size(xf.dtype),
+                               cudaMemcpyDeviceToDevice, s));
+      saved->x.data = cp.get();
+    }
+  }
+}
+
+void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, const LinearP& p,
+                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s) {
+  // linear3d_bwd (cube3d/nn.hpp:99-112): add_vec_bwd then matmul_ab_bwd.
+  if (dy.group != 1 - p.input_group)
+    fail(C3D_ERR_GROUP_MISMATCH, "upstream gradient group does not match the layer output group");
+  Mat dyf = flatten(cube, dy);
+  if (dyf.dirs != saved.x.dirs.swapped())
+    fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB backward must carry the swapped triple");
+  if (db && db->data) {
+    DevBuf cs(static_cast<size_t>(dyf.cols) * sizeof(float), s);
+    k_colsum(dyf.data, dyf.dtype, nullptr, kF32, dyf.rows, dyf.cols, cs.as<float>(), s);
+    Vec out = *db;
+    out.len = dyf.gcols;
+    reduce_to_diagonal(cube, dyf.dirs, cs.as<float>(), 1, &out, s);
+  }
+  Mat da, *dap = nullptr;
+  if (dx && dx->data) {
+    da.data = dx->data;
+    da.dtype = dx->dtype;
+    dap = &da;
+  }
+  ab_backward(cube, mode, dyf, saved.x, p.w, dap, dw, dx_gelu_aux, s);
+  if (dap) *dx = make_act(cube, dx->data, dx->dtype, dy.batch, dy.seq, saved.x.gcols, p.input_group);
+}
+
+// --------------------------------------------------------------- LayerNorm
+
+void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, double eps,
+                   Act& y, LNSaved* saved, cudaStream_t s) {
+  // layernorm3d_fwd (cube3d/nn.hpp:140-185)
+  if (gamma.len != x.hidden || beta.len != x.hidden)
+    fail(C3D_ERR_SHAPE_MISMATCH, "layer norm parameter length does not match hidden size");
+  const Dirs d = triple_for_group(x.group);
+  const int Pout = cube.extent(d.out);
+  const float inv_h = 1.f / static_cast<float>(x.hidden);
+  DevBuf gblock = expand_diagonal(cube, d, gamma, s);
+  DevBuf bblock = expand_diagonal(cube, d, beta, s);
+  y = make_act(cube, y.data, y.dtype, x.batch, x.seq, x.hidden, x.group);
+  DevBuf xhat(x.elems() * dtype_size(x.dtype), s);
+  DevBuf inv_std(static_cast<size_t>(x.rows) * sizeof(float), s);
+  if (Pout == 1) {
+    k_ln_fwd_fused(x.data, x.dtype, x.rows, x.cols, static_cast<float>(eps), gblock.as<float>(),
+                   bblock.as<float>(), y.data, y.dtype, xhat.get(), x.dtype, inv_std.as<float>(), s);
+  } else {
+    DevBuf sums(static_cast<size_t>(x.rows) * sizeof(float), s);
+    DevBuf sq(static_cast<size_t>(x.rows) * sizeof(float), s);
+    k_row_sum(x.data, x.dtype, x.rows, x.cols, nullptr, inv_h, sums.as<float>(), s);
+    cube.all_reduce(d.out, sums.get(), x.rows, kF32, false, s);
+    k_row_sum(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), inv_h, sq.as<float>(), s);
+    cube.all_reduce(d.out, sq.get(), x.rows, kF32, false, s);
+    k_ln_apply(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), sq.as<float>(), inv_h,
+               static_cast<float>(eps), gblock.as<float>(), bblock.as<float>(), y.data, y.dtype,
+               xhat.get(), x.dtype, inv_std.as<float>(), s);
+  }
+  if (saved) {
+    saved->dtype = x.dtype;
+    saved->group = x.group;
+    saved->hidden = x.hidden;
+    saved->xhat = saved->keep(std::move(xhat)).get();
+    saved->inv_std = saved->keep(std::move(inv_std)).as<float>();
+    saved->gamma_block = saved->keep(std::move(gblock)).as<float>();
+  }
+}
+
+void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const Vec* dgamma,
+                   const Vec* dbeta, const void* resid, cudaStream_t s) {
+  // layernorm3d_bwd (cube3d/nn.hpp:187-222)
+  if (dy.group != sv.group || dy.hidden != sv.hidden)
+    fail(C3D_ERR_SHAPE_MISMATCH, "layer norm gradient does not match the saved forward");
+  const Dirs d = triple_for_group(dy.group);
+  const float inv_h = 1.f / static_cast<float>(dy.hidden);
+  if (dgamma && dbeta && dgamma->data && dbeta->data) {
+    DevBuf cs(static_cast<size_t>(2 * dy.cols) * sizeof(float), s);
+    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, cs.as<float>(), s);
+    k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, cs.as<float>() + dy.cols, s);
+    Vec outs[2] = {*dgamma, *dbeta};
+    outs[0].len = outs[1].len = dy.hidden;
+    reduce_to_diagonal(cube, d, cs.as<float>(), 2, outs, s);
+  }
+  DevBuf rs(static_cast<size_t>(2 * dy.rows) * sizeof(float), s);
+  k_ln_bwd_rows(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, dy.rows, dy.cols,
+                rs.as<float>(), s);
+  cube.all_reduce(d.out, rs.get(), 2 * dy.rows, kF32, false, s);
+  dx = make_act(cube, dx.data, dx.dtype, dy.batch, dy.seq, dy.hidden, dy.group);
+  k_ln_bwd_dx(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, sv.inv_std, rs.as<float>(),
+              inv_h, dy.rows, dy.cols, resid, dx.dtype, dx.data, dx.dtype, s);
+}
+
+// --------------------------------------------------------------- attention
+
+namespace {
+
+struct AttnDims {
+  int64_t bl, sl, S, H, dh, ld_qkv, hd;  // hd = H*dh
+  int seq_axis, Ps;
+  float scale;
+};
+
+AttnDims attn_dims(const Cube& cube, const Config& cfg, int group_after_qkv) {
+  // attn_core_dims (cube3d/attention.hpp:66-76)
+  AttnDims a;
+  a.seq_axis = axis_of_group(group_after_qkv);
+  a.Ps = cube.extent(a.seq_axis);
+  const int Ph = cube.extent(axis_of_group(1 - group_after_qkv));
+  if (cfg.heads % Ph)
+    fail(C3D_ERR_HEADS_INDIVISIBLE, "heads=" + std::to_string(cfg.heads) +
+                                        " not divisible by p=" + std::to_string(Ph));
+  a.bl = cfg.batch / cube.extent(kX);
+  a.sl = cfg.seq / a.Ps;
+  a.S = cfg.seq;
+  a.H = cfg.heads / Ph;
+  a.dh = cfg.hidden / cfg.heads;
+  a.hd = a.H * a.dh;
+  a.ld_qkv = 3 * a.hd;
+  a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(a.dh)));
+  return a;
+}
+
+// [batch = (bi, hi)][seq position][dh] views of a packed or gathered [p][rows][H*dh] buffer
+// (queries / context gradient), K-major (rows of dh) or MN-major (dh contiguous, seq as K).
+View packed_view(const void* base, int dtype, const AttnDims& a, bool mn_major) {
+  View v = mn_major ? mk_view(base, dtype, 1, a.hd) : mk_view(base, dtype, a.hd, 1);
+  if (a.Ps > 1) {
+    if (mn_major) v.csplit = a.sl;
+    else v.rsplit = a.sl;
+    v.s_hi = a.bl * a.sl * a.hd;
+  }
+  v.b_lo_n = static_cast<int>(a.H);
+  v.sb_lo = a.dh;
+  v.sb_hi = a.sl * a.hd;
+  return v;
+}
+
+// q (part 0), k (1) or v (2) columns of the local qkv activation, per (bi, hi) slice.
+View qkv_view(const void* qkv, int dtype, const AttnDims& a, int part, bool mn_major) {
+  const void* base = offset(qkv, part * a.dh, dtype);
+  View v = mn_major ? mk_view(base, dtype, 1, a.ld_qkv) : mk_view(base, dtype, a.ld_qkv, 1);
+  v.b_lo_n = static_cast<int>(a.H);
+  v.sb_lo = 3 * a.dh;
+  v.sb_hi = a.sl * a.ld_qkv;
+  return v;
+}
+
+// [slice][S][sl] score / probability buffers.
+View scores_view(const void* base, int dtype, const AttnDims& a, bool transposed) {
+  View v = transposed ? mk_view(base, dtype, 1, a.sl) : mk_view(base, dtype, a.sl, 1);
+  v.b_lo_n = static_cast<int>(a.H);
+  v.sb_lo = a.S * a.sl;
+  v.sb_hi = a.H * a.S * a.sl;
+  return v;
+}
+
+// [p][rows][H*dh] partial (reduce-scatter layout) or the [rows][H*dh] activation itself.
+View packed_out(void* base, int dtype, const AttnDims& a, bool split) {
+  View v = mk_view(base, dtype, a.hd, 1);
+  if (split) {
+    v.rsplit = a.sl;
+    v.s_hi = a.bl * a.sl * a.hd;
+  }
+  v.b_lo_n = static_cast<int>(a.H);
+  v.sb_lo = a.dh;
+  v.sb_hi = a.sl * a.hd;
+  return v;
+}
+
+}  // namespace
+
+void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& qkv_p,
+                   const LinearP& out_p, int& group, Act& y, AttnSaved* sv, bool own_input,
+                   const void* resid, cudaStream_t s) {
+  // attention_fwd (cube3d/attention.hpp:78-136)
+  validate_config(cube, cfg);
+  if (x.hidden != cfg.hidden) fail(C3D_ERR_SHAPE_MISMATCH, "attention input hidden size mismatch");
+  AttnSaved local;
+  AttnSaved& S = sv ? *sv : local;
+  const int dt = x.dtype;
+  const int g_after = 1 - x.group;
+  const ActGeom qg = act_geom(cube.grid(), x.batch, x.seq, 3 * cfg.hidden, g_after);
+  DevBuf& qkv_buf = S.keep(DevBuf(static_cast<size_t>(qg.bl * qg.sl * qg.hl) * dtype_size(dt), s));
+  Act qkv;
+  qkv.data = qkv_buf.get();
+  qkv.dtype = dt;
+  linear_fwd(cube, mode, x, qkv_p, group, qkv, &S.qkv_lin, own_input, LinearEpi{}, s);
+  const AttnDims a = attn_dims(cube, cfg, qkv.group);
+  if (qkv.cols != a.ld_qkv) fail(C3D_ERR_SHAPE_MISMATCH, "qkv projection width mismatch");
+  S.qkv = qkv;
+
+  const int64_t rows = a.bl * a.sl;
+  const int nslices = static_cast<int>(a.bl * a.H);
+  // queries of all local slices: this rank's block, or gathered along the seq axis
+  View qv;
+  if (a.Ps > 1) {
+    DevBuf qloc(static_cast<size_t>(rows * a.hd) * dtype_size(dt), s);
+    k_copy_heads(qkv.data, a.ld_qkv, 3 * a.dh, qloc.get(), a.hd, a.dh, rows, a.H, a.dh, dt, s);
+    DevBuf& qf = S.keep(DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s));
+    cube.all_gather(a.seq_axis, qloc.get(), qf.get(), rows * a.hd, dt, s);
+    S.q_full = qf.get();
+    qv = packed_view(qf.get(), dt, a, false);
+  } else {
+    qv = qkv_view(qkv.data, dt, a, 0, false);
+  }
+  // scores = scale * Q K^T  ([slice][S][sl])
+  DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(nslices * a.S * a.sl) * dtype_size(dt), s));
+  S.probs = pb.get();
+  {
+    Epilogue e;
+    e.out = scores_view(pb.get(), dt, a, false);
+    e.alpha = a.scale;
+    gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, qv, qkv_view(qkv.data, dt, a, 1, false), e, s);
+  }
+  // distributed softmax over the key blocks of the seq axis
+  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
+  if (a.Ps == 1) {
+    k_softmax_fused(pb.get(), dt, srows, a.sl, s);
+  } else {
+    DevBuf mx(static_cast<size_t>(srows) * sizeof(float), s);
+    DevBuf sm(static_cast<size_t>(srows) * sizeof(float), s);
+    k_softmax_rowmax(pb.get(), dt, srows, a.sl, mx.as<float>(), s);
+    cube.all_reduce(a.seq_axis, mx.get(), srows, kF32, true, s);
+    k_softmax_rowexpsum(pb.get(), dt, srows, a.sl, mx.as<float>(), sm.as<float>(), s);
+    cube.all_reduce(a.seq_axis, sm.get(), srows, kF32, false, s);
+    k_softmax_norm(pb.get(), dt, srows, a.sl, mx.as<float>(), sm.as<float>(), s);
+  }
+  // context = P V, reduce-scattered back to this rank's seq block
+  const ActGeom cg = act_geom(cube.grid(), x.batch, x.seq, cfg.hidden, qkv.group);
+  DevBuf& ctx_buf = S.keep(DevBuf(static_cast<size_t>(cg.bl * cg.sl * cg.hl) * dtype_size(dt), s));
+  Act ctx = make_act(cube, ctx_buf.get(), dt, x.batch, x.seq, cfg.hidden, qkv.group);
+  {
+    Epilogue e;
+    DevBuf partial;
+    if (a.Ps == 1) {
+      e.out = packed_out(ctx.data, dt, a, false);
+    } else {
+      partial = DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+      e.out = packed_out(partial.get(), dt, a, true);
+    }
+    gemm_views(cube, mode, a.S, a.dh, a.sl, nslices, scores_view(pb.get(), dt, a, false),
+               qkv_view(qkv.data, dt, a, 2, true), e, s);
+    if (a.Ps > 1) cube.reduce_scatter(a.seq_axis, partial.get(), ctx.data, rows * a.hd, dt, s);
+  }
+  LinearEpi oe;
+  oe.resid = resid;
+  linear_fwd(cube, mode, ctx, out_p, group, y, &S.out_lin, false, oe, s);
+}
+
+void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const AttnSaved& S,
+                   const LinearP& qkv_p, const LinearP& out_p, Act& dx, LayerG& g,
+                   cudaStream_t s) {
+  // attention_bwd (cube3d/attention.hpp:138-189)
+  const int dt = dy.dtype;
+  const ActGeom cg = act_geom(cube.grid(), dy.batch, dy.seq, cfg.hidden, 1 - dy.group);
+  DevBuf dctx_buf(static_cast<size_t>(cg.bl * cg.sl * cg.hl) * dtype_size(dt), s);
+  Act dctx;
+  dctx.data = dctx_buf.get();
+  dctx.dtype = dt;
+  linear_bwd(cube, mode, dy, S.out_lin, out_p, &dctx, &g.w_out, &g.b_out, nullptr, s);
+  const AttnDims a = attn_dims(cube, cfg, dctx.group);
+  const int64_t rows = a.bl * a.sl;
+  const int nslices = static_cast<int>(a.bl * a.H);
+  const void* qkv = S.qkv.data;
+
+  Gathered dcf = gather(cube, a.seq_axis, dctx.data, rows * a.hd, dt, s);
+  DevBuf dqkv_buf(static_cast<size_t>(rows * a.ld_qkv) * dtype_size(dt), s);
+  // dP = dctx_full V^T
+  DevBuf dp(static_cast<size_t>(nslices * a.S * a.sl) * dtype_size(dt), s);
+  {
+    Epilogue e;
+    e.out = scores_view(dp.get(), dt, a, false);
+    gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
+               qkv_view(qkv, dt, a, 2, false), e, s);
+  }
+  // dV = P^T dctx_full
+  {
+    Epilogue e;
+    e.out = qkv_view(dqkv_buf.get(), dt, a, 2, false);
+    gemm_views(cube, mode, a.sl, a.dh, a.S, nslices, scores_view(S.probs, dt, a, true),
+               packed_view(dcf.ptr, dt, a, true), e, s);
+  }
+  // dS = P * (dP - rowdot) * scale, rowdot summed along the seq axis
+  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
+  if (a.Ps == 1) {
+    k_softmax_bwd_fused(dp.get(), S.probs, dt, srows, a.sl, a.scale, s);
+  } else {
+    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
+    k_softmax_bwd_rowdot(dp.get(), S.probs, dt, srows, a.sl, rd.as<float>(), s);
+    cube.all_reduce(a.seq_axis, rd.get(), srows, kF32, false, s);
+    k_softmax_bwd_ds(dp.get(), S.probs, dt, srows, a.sl, rd.as<float>(), a.scale, s);
+  }
+  // dQ = dS K (reduce-scattered), dK = dS^T Q_full
+  {
+    Epilogue e;
+    DevBuf partial;
+    if (a.Ps == 1) {
+      e.out = qkv_view(dqkv_buf.get(), dt, a, 0, false);
+    } else {
+      partial = DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+      e.out = packed_out(partial.get(), dt, a, true);
+    }
+    gemm_views(cube, mode, a.S, a.dh, a.sl, nslices, scores_view(dp.get(), dt, a, false),
+               qkv_view(qkv, dt, a, 1, true), e, s);
+    if (a.Ps > 1) {
+      DevBuf dq(static_cast<size_t>(rows * a.hd) * dtype_size(dt), s);
+      cube.reduce_scatter(a.seq_axis, partial.get(), dq.get(), rows * a.hd, dt, s);
+      k_copy_heads(dq.get(), a.hd, a.dh, dqkv_buf.get(), a.ld_qkv, 3 * a.dh, rows, a.H, a.dh, dt, s);
+    }
+  }
+  {
+    Epilogue e;
+    e.out = qkv_view(dqkv_buf.get(), dt, a, 1, false);
+    const View qv = a.Ps > 1 ? packed_view(S.q_full, dt, a, true) : qkv_view(qkv, dt, a, 0, true);
+    gemm_views(cube, mode, a.sl, a.dh, a.S, nslices, scores_view(dp.get(), dt, a, true), qv, e, s);
+  }
+  Act dqkv = make_act(cube, dqkv_buf.get(), dt, dy.batch, dy.seq, 3 * cfg.hidden, dctx.group);
+  linear_bwd(cube, mode, dqkv, S.qkv_lin, qkv_p, &dx, &g.w_qkv, &g.b_qkv, nullptr, s);
+}
+
+// --------------------------------------------------------------------- MLP
+
+void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& fc1,
+             const LinearP& fc2, int& group, Act& y, MlpSaved* sv, bool own_input,
+             const void* resid, cudaStream_t s) {
+  // mlp_fwd (cube3d/transformer.hpp:44-53); GELU fused into the FC1 epilogue.
+  MlpSaved local;
+  MlpSaved& S = sv ? *sv : local;
+  const int dt = x.dtype;
+  const ActGeom hg = act_geom(cube.grid(), x.batch, x.seq, 4 * cfg.hidden, 1 - x.group);
+  const size_t hbytes = static_cast<size_t>(hg.bl * hg.sl * hg.hl) * dtype_size(dt);
+  Act h1;
+  h1.data = S.keep(DevBuf(hbytes, s)).get();
+  h1.dtype = dt;
+  S.pre_act = S.keep(DevBuf(hbytes, s)).get();
+  LinearEpi e1;
+  e1.act = kActGelu;
+  e1.pre_act = S.pre_act;
+  linear_fwd(cube, mode, x, fc1, group, h1, &S.fc1_lin, own_input, e1, s);
+  LinearEpi e2;
+  e2.resid = resid;
+  linear_fwd(cube, mode, h1, fc2, group, y, &S.fc2_lin, false, e2, s);
+}
+
+void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSaved& S,
+             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s) {
+  // mlp_bwd (cube3d/transformer.hpp:55-70); GELU' fused into the FC2 dX epilogue.
+  const int dt = dy.dtype;
+  const ActGeom hg = act_geom(cube.grid(), dy.batch, dy.seq, 4 * cfg.hidden, 1 - dy.group);
+  DevBuf dh(static_cast<size_t>(hg.bl * hg.sl * hg.hl) * dtype_size(dt), s);
+  Act dh1;
+  dh1.data = dh.get();
+  dh1.dtype = dt;
+  linear_bwd(cube, mode, dy, S.fc2_lin, fc2, &dh1, &g.w_fc2, &g.b_fc2, S.pre_act, s);
+  linear_bwd(cube, mode, dh1, S.fc1_lin, fc1, &dx, &g.w_fc1, &g.b_fc1, nullptr, s);
+}
+
+// ------------------------------------------------------------------- layer
+
+void layer_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LayerP& p, int& group,
+               Act& y, LayerSaved* sv, cudaStream_t s) {
+  // transformer_layer_fwd (cube3d/transformer.hpp:115-128):
+  //   y1 = x + Attn(LN1(x)); y = y1 + MLP(LN2(y1)); residuals fused into the
+  //   OUT and FC2 epilogues.
+  validate_config(cube, cfg);
+  if (x.group != group) fail(C3D_ERR_GROUP_MISMATCH, "activation group does not match state");
+  LayerSaved local;
+  LayerSaved& S = sv ? *sv : local;
+  const int dt = x.dtype;
+  const size_t bytes = x.elems() * dtype_size(dt);
+  Act n1;
+  n1.data = S.keep(DevBuf(bytes, s)).get();
+  n1.dtype = dt;
+  layernorm_fwd(cube, x, p.ln1_g, p.ln1_b, cfg.eps, n1, &S.ln1, s);
+  DevBuf y1buf(bytes, s);
+  Act y1;
+  y1.data = y1buf.get();
+  y1.dtype = dt;
+  attention_fwd(cube, mode, cfg, n1, p.qkv, p.out, group, y1, &S.attn, false, x.data, s);
+  Act n2;
+  n2.data = S.keep(DevBuf(bytes, s)).get();
+  n2.dtype = dt;
+  layernorm_fwd(cube, y1, p.ln2_g, p.ln2_b, cfg.eps, n2, &S.ln2, s);
+  mlp_fwd(cube, mode, cfg, n2, p.fc1, p.fc2, group, y, &S.mlp, false, y1.data, s);
+}
+
+void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const LayerSaved& S,
+               const LayerP& p, Act& dx, LayerG& g, cudaStream_t s) {
+  // transformer_layer_bwd (cube3d/transformer.hpp:130-148)
+  const int dt = dy.dtype;
+  const size_t bytes = dy.elems() * dtype_size(dt);
+  DevBuf dn2b(bytes, s), dy1b(bytes, s), dn1b(bytes, s);
+  Act dn2;
+  dn2.data = dn2b.get();
+  dn2.dtype = dt;
+  mlp_bwd(cube, mode, cfg, dy, S.mlp, p.fc1, p.fc2, dn2, g, s);
+  Act dy1;
+  dy1.data = dy1b.get();
+  dy1.dtype = dt;
+  layernorm_bwd(cube, dn2, S.ln2, dy1, &g.ln2_g, &g.ln2_b, dy.data, s);  // dy1 = dy + LN2'
+  Act dn1;
+  dn1.data = dn1b.get();
+  dn1.dtype = dt;
+  attention_bwd(cube, mode, cfg, dy1, S.attn, p.qkv, p.out, dn1, g, s);
+  layernorm_bwd(cube, dn1, S.ln1, dx, &g.ln1_g, &g.ln1_b, dy1.data, s);  // dx = dy1 + LN1'
+}
+
+}  // namespace c3d

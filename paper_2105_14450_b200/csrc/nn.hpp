@@ -1,0 +1,124 @@
+// 3-D Transformer blocks (cube3d/nn.hpp, cube3d/attention.hpp, cube3d/transformer.hpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <deque>
+#include <memory>
+#include <vector>
+
+#include "ops.hpp"
+
+namespace c3d {
+
+// Activation3D (cube3d/activation.hpp:41-62) with resolved local dims.
+struct Act {
+  void* data = nullptr;
+  int dtype = kBF16;
+  int64_t batch = 0, seq = 0, hidden = 0;
+  int group = 0;
+  int64_t rows = 0, cols = 0;
+  size_t elems() const { return static_cast<size_t>(rows * cols); }
+};
+Act make_act(const Cube& cube, void* data, int dtype, int64_t batch, int64_t seq, int64_t hidden,
+             int group);
+Mat flatten(const Cube& cube, const Act& a);
+
+struct Config {
+  int64_t batch = 0, seq = 0, heads = 0, hidden = 0;
+  double eps = 1e-5;
+};
+void validate_config(const Cube& cube, const Config& cfg);
+
+struct LinearP {
+  Mat w;
+  Vec b;
+  int input_group = 0;
+};
+
+// Saved-for-backward state: owns its device buffers.
+struct Saved {
+  virtual ~Saved() = default;
+  std::deque<DevBuf> bufs;  // deque: references stay valid as buffers are added
+  DevBuf& keep(DevBuf&& b) {
+    bufs.push_back(std::move(b));
+    return bufs.back();
+  }
+};
+
+struct LinearSaved : Saved {
+  Mat x;  // flattened forward input (LinearSaved::x_flat, cube3d/nn.hpp:69-72)
+};
+struct LNSaved : Saved {
+  void* xhat = nullptr;
+  int dtype = kBF16;
+  float* inv_std = nullptr;
+  float* gamma_block = nullptr;
+  int group = 0;
+  int64_t hidden = 0;
+};
+struct AttnSaved : Saved {
+  LinearSaved qkv_lin, out_lin;
+  Act qkv;                 // (b/px)(s/p_s) x 3h/p_h, head-major [head][q|k|v][dim]
+  void* q_full = nullptr;  // gathered queries [p_s][rows][H*dh] (p_s > 1)
+  void* probs = nullptr;   // [b_loc*H][s][s_loc]
+};
+struct MlpSaved : Saved {
+  LinearSaved fc1_lin, fc2_lin;
+  void* pre_act = nullptr;
+};
+struct LayerSaved : Saved {
+  LNSaved ln1, ln2;
+  AttnSaved attn;
+  MlpSaved mlp;
+};
+
+struct LayerP {
+  Vec ln1_g, ln1_b;
+  LinearP qkv, out;
+  Vec ln2_g, ln2_b;
+  LinearP fc1, fc2;
+};
+struct LayerG {  // gradients (outputs), same shapes as LayerP
+  Vec ln1_g, ln1_b;
+  Mat w_qkv;
+  Vec b_qkv;
+  Mat w_out;
+  Vec b_out;
+  Vec ln2_g, ln2_b;
+  Mat w_fc1;
+  Vec b_fc1;
+  Mat w_fc2;
+  Vec b_fc2;
+};
+
+// `own_input`: copy x into the saved state (standalone API); otherwise keep a view
+// (the caller guarantees x outlives backward, as inside a layer).
+void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group, Act& y,
+                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s);
+void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, const LinearP& p,
+                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s);
+
+void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, double eps,
+                   Act& y, LNSaved* saved, cudaStream_t s);
+void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& saved, Act& dx, const Vec* dgamma,
+                   const Vec* dbeta, const void* resid, cudaStream_t s);
+
+void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& qkv,
+                   const LinearP& out, int& group, Act& y, AttnSaved* saved, bool own_input,
+                   const void* resid, cudaStream_t s);
+void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const AttnSaved& sv,
+                   const LinearP& qkv, const LinearP& out, Act& dx, LayerG& g, cudaStream_t s);
+
+void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& fc1,
+             const LinearP& fc2, int& group, Act& y, MlpSaved* saved, bool own_input,
+             const void* resid, cudaStream_t s);
+void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSaved& sv,
+             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s);
+
+void layer_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LayerP& p, int& group,
+               Act& y, LayerSaved* saved, cudaStream_t s);
+void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const LayerSaved& sv,
+               const LayerP& p, Act& dx, LayerG& g, cudaStream_t s);
+
+}  // namespace c3d

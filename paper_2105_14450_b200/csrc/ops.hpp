@@ -1,0 +1,91 @@
+// 3-D parallel operators (cube3d/ops3d.hpp) over device-resident shards.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "cube.hpp"
+#include "gemm.hpp"
+#include "grid.hpp"
+
+namespace c3d {
+
+void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s);
+
+// One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
+void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
+                const View& b, const Epilogue& e, cudaStream_t s);
+
+// ShardedMatrix with its local shard dims resolved (cube3d/sharding.hpp:18-34).
+struct Mat {
+  void* data = nullptr;
+  int dtype = kBF16;
+  int64_t grows = 0, gcols = 0;
+  int layout = kInput;
+  Dirs dirs;
+  int64_t rows = 0, cols = 0;  // local shard
+  size_t elems() const { return static_cast<size_t>(rows * cols); }
+};
+
+Mat make_mat(const Cube& cube, void* data, int dtype, int64_t grows, int64_t gcols, int layout,
+             const Dirs& dirs);
+Mat from_c(const Cube& cube, const c3d_matrix& m);
+void to_c(const Mat& m, c3d_matrix* out);
+
+// DiagonalVector (cube3d/sharding.hpp:38-47).
+struct Vec {
+  void* data = nullptr;
+  int dtype = kF32;
+  int64_t len = 0;
+};
+
+// Device buffer holding the gathered operand, or the shard itself when the axis
+// has extent 1.
+struct Gathered {
+  DevBuf buf;
+  const void* ptr = nullptr;
+};
+Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype, cudaStream_t s);
+
+// expand_diagonal (cube3d/ops3d.hpp:291-310): fp32 column block of length len/p_out
+// for an operand with triple d. Returns a stream-ordered fp32 buffer.
+DevBuf expand_diagonal(Cube& cube, const Dirs& d, const Vec& v, cudaStream_t s);
+// reduce_to_diagonal (cube3d/ops3d.hpp:315-336) of `nvec` packed fp32 column-sum vectors
+// (each of length len/p_out) into the vectors out[0..nvec) on holder ranks.
+void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nvec,
+                        const Vec* outs, cudaStream_t s);
+
+void matmul_ab_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s);
+void matmul_ab_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                   Mat& db, cudaStream_t s);
+void matmul_abt_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s);
+void matmul_abt_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                    Mat& db, cudaStream_t s);
+void matmul_atb_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s);
+void matmul_atb_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                    Mat& db, cudaStream_t s);
+
+void add_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s);
+void add_vec_bwd(Cube& cube, const Mat& dc, Mat& da, const Vec& db, cudaStream_t s);
+void mul_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s);
+void mul_vec_bwd(Cube& cube, const Mat& dc, const Mat& a, const Vec& b, Mat& da, const Vec& db,
+                 cudaStream_t s);
+
+// Linear-layer building block shared by matmul_ab_fwd and linear3d_fwd: C = A B with an
+// optional fused epilogue (bias already expanded, activation, residual).
+struct LinearEpi {
+  const float* bias = nullptr;  // expanded column block (len = C local cols)
+  int act = kActNone;
+  void* pre_act = nullptr;      // stores pre-activation (C layout)
+  const void* resid = nullptr;  // C layout, C dtype
+};
+void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& epi,
+                cudaStream_t s);
+// dA = dC B^T (RS along d.in), dB = A^T dC (RS along x); either output may be skipped
+// (data == nullptr). `da_epi_aux`: if set, dA *= gelu'(aux) is fused (aux in dA layout).
+void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
+                 Mat* db, const void* da_gelu_aux, cudaStream_t s);
+
+}  // namespace c3d

@@ -1,0 +1,521 @@
+// 3-D matmul and matrix-vector operators (cube3d/ops3d.hpp), executed per rank
+// as: NCCL all-gathers along the operand axes -> one local GEMM whose operand
+// views address the gathered buffers in place (no gather_cols reorder, no
+// transposes) -> NCCL reduce-scatter along the result axis -> fused epilogue.
+#include <string>
+
+#include "common.hpp"
+#include "kernels.hpp"
+#include "ops.hpp"
+
+namespace c3d {
+
+namespace {
+
+bool input_family(const Mat& m) { return m.layout == kInput || m.layout == kOutput; }
+
+void require_input_family(const Mat& m, const char* what) {
+  if (!input_family(m))
+    fail(C3D_ERR_SHAPE_MISMATCH, std::string(what) + " must be in the Input/Output family, got " +
+                                     layout_name(m.layout));
+}
+
+View kmajor(const void* p, int dtype, int64_t ld) {
+  View v;
+  v.base = const_cast<void*>(p);
+  v.dtype = dtype;
+  v.sr = ld;
+  v.sc = 1;
+  return v;
+}
+View mnmajor(const void* p, int dtype, int64_t ld) {
+  View v;
+  v.base = const_cast<void*>(p);
+  v.dtype = dtype;
+  v.sr = 1;
+  v.sc = ld;
+  return v;
+}
+View out_view(void* p, int dtype, int64_t ld) {
+  View v;
+  v.base = p;
+  v.dtype = dtype;
+  v.sr = ld;
+  v.sc = 1;
+  return v;
+}
+
+void local_gemm(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, const View& a,
+                const View& b, const Epilogue& e, cudaStream_t s) {
+  GemmProblem p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.a = a;
+  p.b = b;
+  p.epi = e;
+  run_gemm(p, mode, cube.num_sms(), s);
+  cube.add_madds(static_cast<uint64_t>(M) * N * K);
+}
+
+}  // namespace
+
+void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
+                const View& b, const Epilogue& e, cudaStream_t s) {
+  GemmProblem p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.batch = batch;
+  p.a = a;
+  p.b = b;
+  p.epi = e;
+  run_gemm(p, mode, cube.num_sms(), s);
+  cube.add_madds(static_cast<uint64_t>(batch) * M * N * K);
+}
+
+Mat make_mat(const Cube& cube, void* data, int dtype, int64_t grows, int64_t gcols, int layout,
+             const Dirs& dirs) {
+  Mat m;
+  m.data = data;
+  m.dtype = dtype;
+  m.grows = grows;
+  m.gcols = gcols;
+  m.layout = layout;
+  m.dirs = dirs;
+  if (dtype != kF32 && dtype != kBF16) fail(C3D_ERR_CONFIG_INVALID, "unknown dtype");
+  const Bounds b = shard_bounds(layout, cube.grid(), cube.coords(), grows, gcols, dirs);
+  m.rows = b.rows.size();
+  m.cols = b.cols.size();
+  return m;
+}
+
+Mat from_c(const Cube& cube, const c3d_matrix& m) {
+  Dirs d{m.dirs[0], m.dirs[1], m.dirs[2]};
+  if (m.layout < 0 || m.layout > 3) fail(C3D_ERR_SHAPE_MISMATCH, "unknown layout");
+  return make_mat(cube, m.data, m.dtype, m.global_rows, m.global_cols, m.layout, d);
+}
+
+void to_c(const Mat& m, c3d_matrix* out) {
+  out->data = m.data;
+  out->dtype = m.dtype;
+  out->global_rows = m.grows;
+  out->global_cols = m.gcols;
+  out->layout = m.layout;
+  out->dirs[0] = m.dirs.in;
+  out->dirs[1] = m.dirs.w;
+  out->dirs[2] = m.dirs.out;
+}
+
+Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype,
+                cudaStream_t s) {
+  Gathered g;
+  const int p = cube.extent(axis);
+  if (p == 1) {
+    g.ptr = shard;
+    return g;
+  }
+  g.buf = DevBuf(count * p * dtype_size(dtype), s);
+  cube.all_gather(axis, shard, g.buf.get(), count, dtype, s);
+  g.ptr = g.buf.get();
+  return g;
+}
+
+// ---------------------------------------------------------------- vectors
+
+DevBuf expand_diagonal(Cube& cube, const Dirs& d, const Vec& v, cudaStream_t s) {
+  const Grid& g = cube.grid();
+  const Range sl = diagonal_slice(g, cube.coords(), v.len);
+  const int64_t n2 = sl.size();
+  const int px = g.dims[kX];
+  if (g.dims[d.in] != g.dims[d.out])
+    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need equal input/output axis extents");
+  DevBuf out(static_cast<size_t>(n2 * px) * sizeof(float), s);
+  if (g.size() == 1) {
+    k_convert(v.data, v.dtype, out.get(), kF32, n2, s);
+    return out;
+  }
+  // broadcast the holder's slice along the operand's input axis from position
+  // owner[d.out] (the diagonal rank of that line), then all-gather along x.
+  DevBuf piece(static_cast<size_t>(n2) * dtype_size(v.dtype), s);
+  if (diagonal_holder(cube.coords()))
+    C3D_CUDA(cudaMemcpyAsync(piece.get(), v.data, n2 * dtype_size(v.dtype),
+                             cudaMemcpyDeviceToDevice, s));
+  cube.broadcast(d.in, cube.coord(d.out), piece.get(), n2, v.dtype, s);
+  if (px == 1) {
+    k_convert(piece.get(), v.dtype, out.get(), kF32, n2, s);
+    return out;
+  }
+  DevBuf full(static_cast<size_t>(n2 * px) * dtype_size(v.dtype), s);
+  cube.all_gather(kX, piece.get(), full.get(), n2, v.dtype, s);
+  k_convert(full.get(), v.dtype, out.get(), kF32, n2 * px, s);
+  return out;
+}
+
+void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nvec,
+                        const Vec* outs, cudaStream_t s) {
+  const Grid& g = cube.grid();
+  const int64_t len = outs[0].len;
+  const Range sl = diagonal_slice(g, cube.coords(), len);
+  const int64_t n2 = sl.size();
+  const int px = g.dims[kX];
+  const int64_t block = n2 * px;  // per-vector column-sum length (len / p_out)
+  const bool holder = diagonal_holder(cube.coords());
+  if (g.size() == 1) {
+    for (int k = 0; k < nvec; ++k) k_convert(colsums + k * block, kF32, outs[k].data, outs[k].dtype, n2, s);
+    return;
+  }
+  // reduce-scatter along x: each vector's block splits into px slices; pack the
+  // slices position-major so one collective serves all vectors.
+  DevBuf packed(static_cast<size_t>(nvec * block) * sizeof(float), s);
+  for (int q = 0; q < px; ++q)
+    for (int k = 0; k < nvec; ++k)
+      C3D_CUDA(cudaMemcpyAsync(packed.as<float>() + (q * nvec + k) * n2,
+                               colsums + k * block + q * n2, n2 * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s));
+  DevBuf slice(static_cast<size_t>(nvec * n2) * sizeof(float), s);
+  cube.reduce_scatter(kX, packed.get(), slice.get(), nvec * n2, kF32, s);
+  // sum along the operand's input axis (adjoint of the forward broadcast)
+  cube.all_reduce(d.in, slice.get(), nvec * n2, kF32, false, s);
+  if (holder)
+    for (int k = 0; k < nvec; ++k)
+      k_convert(slice.as<float>() + k * n2, kF32, outs[k].data, outs[k].dtype, n2, s);
+}
+
+void add_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s) {
+  require_input_family(a, "A");
+  if (b.len != a.gcols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "vector length " + std::to_string(b.len) +
+                                     " does not match matrix cols " + std::to_string(a.gcols));
+  DevBuf bias = expand_diagonal(cube, a.dirs, b, s);
+  c = make_mat(cube, c.data, c.dtype, a.grows, a.gcols, a.layout, a.dirs);
+  Epilogue e;
+  e.out = out_view(c.data, c.dtype, c.cols);
+  e.bias = bias.as<float>();
+  k_apply_epilogue(a.data, a.dtype, a.rows, a.cols, e, s);
+}
+
+void add_vec_bwd(Cube& cube, const Mat& dc, Mat& da, const Vec& db, cudaStream_t s) {
+  require_input_family(dc, "dC");
+  DevBuf cs(static_cast<size_t>(dc.cols) * sizeof(float), s);
+  k_colsum(dc.data, dc.dtype, nullptr, kF32, dc.rows, dc.cols, cs.as<float>(), s);
+  da = make_mat(cube, da.data, da.dtype, dc.grows, dc.gcols, dc.layout, dc.dirs);
+  if (da.data != dc.data) k_convert(dc.data, dc.dtype, da.data, da.dtype, dc.elems(), s);
+  Vec out = db;
+  out.len = dc.gcols;
+  reduce_to_diagonal(cube, dc.dirs, cs.as<float>(), 1, &out, s);
+}
+
+void mul_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s) {
+  require_input_family(a, "A");
+  if (b.len != a.gcols) fail(C3D_ERR_SHAPE_MISMATCH, "vector length does not match matrix cols");
+  DevBuf scale = expand_diagonal(cube, a.dirs, b, s);
+  c = make_mat(cube, c.data, c.dtype, a.grows, a.gcols, a.layout, a.dirs);
+  k_mul_cols(a.data, a.dtype, scale.as<float>(), c.data, c.dtype, a.rows, a.cols, s);
+}
+
+void mul_vec_bwd(Cube& cube, const Mat& dc, const Mat& a, const Vec& b, Mat& da, const Vec& db,
+                 cudaStream_t s) {
+  require_input_family(dc, "dC");
+  if (dc.rows != a.rows || dc.cols != a.cols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "dC shape does not match the forward input");
+  DevBuf cs(static_cast<size_t>(dc.cols) * sizeof(float), s);
+  k_colsum(dc.data, dc.dtype, a.data, a.dtype, dc.rows, dc.cols, cs.as<float>(), s);
+  DevBuf scale = expand_diagonal(cube, a.dirs, b, s);
+  da = make_mat(cube, da.data, da.dtype, dc.grows, dc.gcols, dc.layout, dc.dirs);
+  k_mul_cols(dc.data, dc.dtype, scale.as<float>(), da.data, da.dtype, dc.rows, dc.cols, s);
+  Vec out = db;
+  out.len = dc.gcols;
+  reduce_to_diagonal(cube, dc.dirs, cs.as<float>(), 1, &out, s);
+}
+
+// ---------------------------------------------------------------- C = A B
+
+void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& le,
+                cudaStream_t s) {
+  const Dirs d = a.dirs;
+  const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
+  // a: (M/(Pw Pin)) x (N/Pout); b: (N/Pout) x (K/(Pin Pw))
+  Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+  Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);   // [Pw][N/Pout][K/(Pin Pw)]
+  const int64_t Mg = a.rows * Pin, Kg = a.cols, Ng = b.cols * Pw;
+  View av = kmajor(af.ptr, a.dtype, a.cols);
+  View bv = mnmajor(bf.ptr, b.dtype, b.cols);
+  if (Pw > 1) {
+    bv.rsplit = b.cols;
+    bv.s_hi = b.rows * b.cols;
+  }
+  c = make_mat(cube, c.data, c.dtype, a.grows, b.gcols, kOutput, d.swapped());
+  Epilogue e;
+  if (Pout == 1) {
+    e.out = out_view(c.data, c.dtype, c.cols);
+    e.bias = le.bias;
+    e.act = le.act;
+    e.pre_act = le.pre_act;
+    e.pre_dtype = c.dtype;
+    e.resid = le.resid;
+    e.resid_dtype = c.dtype;
+    local_gemm(cube, mode, Mg, Ng, Kg, av, bv, e, s);
+    return;
+  }
+  DevBuf partial(static_cast<size_t>(Mg * Ng) * dtype_size(c.dtype), s);
+  e.out = out_view(partial.get(), c.dtype, Ng);
+  local_gemm(cube, mode, Mg, Ng, Kg, av, bv, e, s);
+  cube.reduce_scatter(d.out, partial.get(), c.data, c.elems(), c.dtype, s);
+  if (le.bias || le.act != kActNone || le.resid) {
+    Epilogue f;
+    f.out = out_view(c.data, c.dtype, c.cols);
+    f.bias = le.bias;
+    f.act = le.act;
+    f.pre_act = le.pre_act;
+    f.pre_dtype = c.dtype;
+    f.resid = le.resid;
+    f.resid_dtype = c.dtype;
+    k_apply_epilogue(c.data, c.dtype, c.rows, c.cols, f, s);
+  }
+}
+
+void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
+                 Mat* db, const void* da_gelu_aux, cudaStream_t s) {
+  const Dirs d = a.dirs;
+  const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
+  // dC: (M/(Pw Pout)) x (K/Pin) with triple d.swapped(): gather along d.out
+  Gathered dcf = gather(cube, d.out, dc.data, dc.elems(), dc.dtype, s);  // (M/Pw) x (K/Pin)
+  const int64_t Mrows = dc.rows * Pout, Kc = dc.cols;
+  if (da && da->data) {
+    Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);
+    *da = make_mat(cube, da->data, da->dtype, a.grows, a.gcols, a.layout, a.dirs);
+    // partial dA (M/Pw) x (N/Pout) = dc_full * b_full^T
+    View av = kmajor(dcf.ptr, dc.dtype, Kc);
+    View bv = kmajor(bf.ptr, b.dtype, b.cols);
+    if (Pw > 1) {
+      bv.csplit = b.cols;
+      bv.s_hi = b.rows * b.cols;
+    }
+    Epilogue e;
+    if (Pin == 1) {
+      e.out = out_view(da->data, da->dtype, da->cols);
+      if (da_gelu_aux) {
+        e.act = kActGeluGrad;
+        e.aux = da_gelu_aux;
+        e.aux_dtype = da->dtype;
+      }
+      local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
+    } else {
+      DevBuf partial(static_cast<size_t>(Mrows * b.rows) * dtype_size(da->dtype), s);
+      e.out = out_view(partial.get(), da->dtype, b.rows);
+      local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
+      cube.reduce_scatter(d.in, partial.get(), da->data, da->elems(), da->dtype, s);
+      if (da_gelu_aux) {
+        Epilogue f;
+        f.out = out_view(da->data, da->dtype, da->cols);
+        f.act = kActGeluGrad;
+        f.aux = da_gelu_aux;
+        f.aux_dtype = da->dtype;
+        k_apply_epilogue(da->data, da->dtype, da->rows, da->cols, f, s);
+      }
+    }
+  }
+  if (db && db->data) {
+    Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+    *db = make_mat(cube, db->data, db->dtype, b.grows, b.gcols, kWeight, d);
+    // partial dB[k_in][n] = sum_m a_full[m][k_in] dc_full[m][n], written column-block-major
+    // [Pw][N/Pout][K/(Pin Pw)] so the reduce-scatter along x lands each rank's shard.
+    View av = mnmajor(af.ptr, a.dtype, a.cols);
+    View bv = mnmajor(dcf.ptr, dc.dtype, Kc);
+    Epilogue e;
+    if (Pw == 1) {
+      e.out = out_view(db->data, db->dtype, db->cols);
+      local_gemm(cube, mode, a.cols, Kc, Mrows, av, bv, e, s);
+    } else {
+      DevBuf partial(static_cast<size_t>(a.cols * Kc) * dtype_size(db->dtype), s);
+      e.out = out_view(partial.get(), db->dtype, db->cols);
+      e.out.csplit = db->cols;
+      e.out.s_hi = db->rows * db->cols;
+      local_gemm(cube, mode, a.cols, Kc, Mrows, av, bv, e, s);
+      cube.reduce_scatter(d.w, partial.get(), db->data, db->elems(), db->dtype, s);
+    }
+  }
+}
+
+void matmul_ab_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s) {
+  require_input_family(a, "A");
+  if (b.layout != kWeight) fail(C3D_ERR_SHAPE_MISMATCH, "B of C=AB must be Weight layout");
+  if (a.dirs != b.dirs)
+    fail(C3D_ERR_DIRECTION_CLASH, "A and B of C=AB must share one direction triple");
+  if (a.gcols != b.grows)
+    fail(C3D_ERR_SHAPE_MISMATCH, "C=AB needs A cols == B rows, got " + std::to_string(a.gcols) +
+                                     " vs " + std::to_string(b.grows));
+  ab_forward(cube, mode, a, b, c, LinearEpi{}, s);
+}
+
+void matmul_ab_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                   Mat& db, cudaStream_t s) {
+  require_input_family(dc, "dC");
+  if (dc.dirs != a.dirs.swapped())
+    fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB backward must carry the swapped triple");
+  if (dc.grows != a.grows || dc.gcols != b.gcols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "dC shape does not match the forward output");
+  ab_backward(cube, mode, dc, a, b, &da, &db, nullptr, s);
+}
+
+// ---------------------------------------------------------------- C = A B^T
+
+void matmul_abt_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s) {
+  require_input_family(a, "A");
+  if (b.layout != kWeightOfTranspose)
+    fail(C3D_ERR_SHAPE_MISMATCH, "B of C=AB^T must be WeightOfTranspose layout");
+  if (a.dirs != b.dirs)
+    fail(C3D_ERR_DIRECTION_CLASH, "A and B of C=AB^T must share one direction triple");
+  if (a.gcols != b.gcols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "C=AB^T needs A cols == B cols, got " +
+                                     std::to_string(a.gcols) + " vs " + std::to_string(b.gcols));
+  const Dirs d = a.dirs;
+  const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
+  Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+  Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);   // (K/Pin) x (N/Pout)
+  const int64_t Mg = a.rows * Pin, Ng = b.rows * Pw, Kg = a.cols;
+  c = make_mat(cube, c.data, c.dtype, a.grows, b.grows, kOutput, d.swapped());
+  Epilogue e;
+  DevBuf partial;
+  if (Pout == 1) {
+    e.out = out_view(c.data, c.dtype, c.cols);
+  } else {
+    partial = DevBuf(static_cast<size_t>(Mg * Ng) * dtype_size(c.dtype), s);
+    e.out = out_view(partial.get(), c.dtype, Ng);
+  }
+  local_gemm(cube, mode, Mg, Ng, Kg, kmajor(af.ptr, a.dtype, a.cols), kmajor(bf.ptr, b.dtype, b.cols),
+             e, s);
+  if (Pout > 1) cube.reduce_scatter(d.out, partial.get(), c.data, c.elems(), c.dtype, s);
+}
+
+void matmul_abt_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                    Mat& db, cudaStream_t s) {
+  require_input_family(dc, "dC");
+  if (dc.dirs != a.dirs.swapped())
+    fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB^T backward must carry the swapped triple");
+  if (dc.grows != a.grows || dc.gcols != b.grows)
+    fail(C3D_ERR_SHAPE_MISMATCH, "dC shape does not match the forward output");
+  const Dirs d = a.dirs;
+  const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
+  Gathered dcf = gather(cube, d.out, dc.data, dc.elems(), dc.dtype, s);  // (M/Pw) x (K/Pin)
+  Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);       // (K/Pin) x (N/Pout)
+  const int64_t Mrows = dc.rows * Pout, Kc = dc.cols;
+  {
+    da = make_mat(cube, da.data, da.dtype, a.grows, a.gcols, a.layout, a.dirs);
+    Epilogue e;
+    DevBuf partial;
+    if (Pin == 1) {
+      e.out = out_view(da.data, da.dtype, da.cols);
+    } else {
+      partial = DevBuf(static_cast<size_t>(Mrows * b.cols) * dtype_size(da.dtype), s);
+      e.out = out_view(partial.get(), da.dtype, b.cols);
+    }
+    local_gemm(cube, mode, Mrows, b.cols, Kc, kmajor(dcf.ptr, dc.dtype, Kc),
+               mnmajor(bf.ptr, b.dtype, b.cols), e, s);
+    if (Pin > 1) cube.reduce_scatter(d.in, partial.get(), da.data, da.elems(), da.dtype, s);
+  }
+  {
+    Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+    db = make_mat(cube, db.data, db.dtype, b.grows, b.gcols, kWeightOfTranspose, d);
+    Epilogue e;
+    DevBuf partial;
+    if (Pw == 1) {
+      e.out = out_view(db.data, db.dtype, db.cols);
+    } else {
+      partial = DevBuf(static_cast<size_t>(Kc * a.cols) * dtype_size(db.dtype), s);
+      e.out = out_view(partial.get(), db.dtype, a.cols);
+    }
+    // partial (K/Pin) x (N/Pout) = dc_full^T a_full
+    local_gemm(cube, mode, Kc, a.cols, Mrows, mnmajor(dcf.ptr, dc.dtype, Kc),
+               mnmajor(af.ptr, a.dtype, a.cols), e, s);
+    if (Pw > 1) cube.reduce_scatter(d.w, partial.get(), db.data, db.elems(), db.dtype, s);
+  }
+}
+
+// ---------------------------------------------------------------- C = A^T B
+
+void matmul_atb_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s) {
+  require_input_family(a, "A");
+  require_input_family(b, "B");
+  if (b.dirs != a.dirs.swapped())
+    fail(C3D_ERR_DIRECTION_CLASH, "B of C=A^TB must carry A's swapped triple");
+  if (a.grows != b.grows)
+    fail(C3D_ERR_SHAPE_MISMATCH, "C=A^TB needs A rows == B rows, got " +
+                                     std::to_string(a.grows) + " vs " + std::to_string(b.grows));
+  const Dirs d = a.dirs;
+  const int Pw = cube.extent(d.w);
+  Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);   // (M/Pw) x (N/Pout)
+  Gathered bf = gather(cube, d.out, b.data, b.elems(), b.dtype, s);  // (M/Pw) x (K/Pin)
+  const int64_t Mrows = a.rows * cube.extent(d.in);
+  c = make_mat(cube, c.data, c.dtype, a.gcols, b.gcols, kWeight, d);
+  const int64_t Kc = b.cols;
+  Epilogue e;
+  DevBuf partial;
+  if (Pw == 1) {
+    e.out = out_view(c.data, c.dtype, c.cols);
+  } else {
+    partial = DevBuf(static_cast<size_t>(a.cols * Kc) * dtype_size(c.dtype), s);
+    e.out = out_view(partial.get(), c.dtype, c.cols);
+    e.out.csplit = c.cols;
+    e.out.s_hi = c.rows * c.cols;
+  }
+  local_gemm(cube, mode, a.cols, Kc, Mrows, mnmajor(af.ptr, a.dtype, a.cols),
+             mnmajor(bf.ptr, b.dtype, Kc), e, s);
+  if (Pw > 1) cube.reduce_scatter(d.w, partial.get(), c.data, c.elems(), c.dtype, s);
+}
+
+void matmul_atb_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
+                    Mat& db, cudaStream_t s) {
+  if (dc.layout != kWeight)
+    fail(C3D_ERR_SHAPE_MISMATCH, "dC of C=A^TB backward must be Weight layout");
+  if (dc.dirs != a.dirs) fail(C3D_ERR_DIRECTION_CLASH, "dC of C=A^TB backward must carry A's triple");
+  if (dc.grows != a.gcols || dc.gcols != b.gcols)
+    fail(C3D_ERR_SHAPE_MISMATCH, "dC shape does not match the forward output");
+  const Dirs d = a.dirs;
+  const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
+  Gathered dcf = gather(cube, d.w, dc.data, dc.elems(), dc.dtype, s);  // [Pw][N/Pout][K/(Pin Pw)]
+  const int64_t Kc = dc.cols * Pw;
+  {
+    Gathered bf = gather(cube, d.out, b.data, b.elems(), b.dtype, s);  // (M/Pw) x (K/Pin)
+    const int64_t Mrows = b.rows * Pout;
+    da = make_mat(cube, da.data, da.dtype, a.grows, a.gcols, a.layout, a.dirs);
+    View bv = kmajor(dcf.ptr, dc.dtype, dc.cols);
+    if (Pw > 1) {
+      bv.csplit = dc.cols;
+      bv.s_hi = dc.rows * dc.cols;
+    }
+    Epilogue e;
+    DevBuf partial;
+    if (Pin == 1) {
+      e.out = out_view(da.data, da.dtype, da.cols);
+    } else {
+      partial = DevBuf(static_cast<size_t>(Mrows * dc.rows) * dtype_size(da.dtype), s);
+      e.out = out_view(partial.get(), da.dtype, dc.rows);
+    }
+    local_gemm(cube, mode, Mrows, dc.rows, Kc, kmajor(bf.ptr, b.dtype, b.cols), bv, e, s);
+    if (Pin > 1) cube.reduce_scatter(d.in, partial.get(), da.data, da.elems(), da.dtype, s);
+  }
+  {
+    Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+    const int64_t Mrows = a.rows * Pin;
+    db = make_mat(cube, db.data, db.dtype, b.grows, b.gcols, b.layout, b.dirs);
+    View bv = mnmajor(dcf.ptr, dc.dtype, dc.cols);
+    if (Pw > 1) {
+      bv.rsplit = dc.cols;
+      bv.s_hi = dc.rows * dc.cols;
+    }
+    Epilogue e;
+    DevBuf partial;
+    if (Pout == 1) {
+      e.out = out_view(db.data, db.dtype, db.cols);
+    } else {
+      partial = DevBuf(static_cast<size_t>(Mrows * Kc) * dtype_size(db.dtype), s);
+      e.out = out_view(partial.get(), db.dtype, Kc);
+    }
+    local_gemm(cube, mode, Mrows, Kc, a.cols, kmajor(af.ptr, a.dtype, a.cols), bv, e, s);
+    if (Pout > 1) cube.reduce_scatter(d.out, partial.get(), db.data, db.elems(), db.dtype, s);
+  }
+}
+
+}  // namespace c3d
