@@ -179,97 +179,6 @@ __global__ void ln_bwd_dx_kernel(const void* dy, int dt, const void* xhat, int x
   }
 }
 
-// ------------------------------------------------------------ softmax
-__global__ void softmax_rowmax_kernel(const void* sc, int dt, int64_t rows, int64_t cols,
-                                      float* mx) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  float m = -INFINITY;
-  for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, ld_any(sc, dt, r * cols + c));
-  m = warp_max(m);
-  if (lane == 0) mx[r] = m;
-}
-
-__global__ void softmax_rowexpsum_kernel(const void* sc, int dt, int64_t rows, int64_t cols,
-                                         const float* mx, float* sum) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  const float m = mx[r];
-  float s = 0.f;
-  for (int64_t c = lane; c < cols; c += 32) s += expf(ld_any(sc, dt, r * cols + c) - m);
-  s = warp_sum(s);
-  if (lane == 0) sum[r] = s;
-}
-
-__global__ void softmax_norm_kernel(void* sc, int dt, int64_t rows, int64_t cols,
-                                    const float* mx, const float* sum) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  const float m = mx[r], inv = 1.f / sum[r];
-  for (int64_t c = lane; c < cols; c += 32) {
-    const int64_t o = r * cols + c;
-    st_any(sc, dt, o, expf(ld_any(sc, dt, o) - m) * inv);
-  }
-}
-
-__global__ void softmax_fused_kernel(void* sc, int dt, int64_t rows, int64_t cols) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  float m = -INFINITY;
-  for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, ld_any(sc, dt, r * cols + c));
-  m = warp_max(m);
-  float s = 0.f;
-  for (int64_t c = lane; c < cols; c += 32) s += expf(ld_any(sc, dt, r * cols + c) - m);
-  const float inv = 1.f / warp_sum(s);
-  for (int64_t c = lane; c < cols; c += 32) {
-    const int64_t o = r * cols + c;
-    st_any(sc, dt, o, expf(ld_any(sc, dt, o) - m) * inv);
-  }
-}
-
-__global__ void softmax_bwd_rowdot_kernel(const void* dp, const void* p, int dt, int64_t rows,
-                                          int64_t cols, float* rowdot) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  float s = 0.f;
-  for (int64_t c = lane; c < cols; c += 32)
-    s += ld_any(dp, dt, r * cols + c) * ld_any(p, dt, r * cols + c);
-  s = warp_sum(s);
-  if (lane == 0) rowdot[r] = s;
-}
-
-__global__ void softmax_bwd_ds_kernel(void* dp, const void* p, int dt, int64_t rows,
-                                      int64_t cols, const float* rowdot, float scale) {
-  const int64_t n = rows * cols;
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = t / cols;
-    const float pv = ld_any(p, dt, t);
-    st_any(dp, dt, t, pv * (ld_any(dp, dt, t) - rowdot[r]) * scale);
-  }
-}
-
-__global__ void softmax_bwd_fused_kernel(void* dp, const void* p, int dt, int64_t rows,
-                                         int64_t cols, float scale) {
-  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (r >= rows) return;
-  float s = 0.f;
-  for (int64_t c = lane; c < cols; c += 32)
-    s += ld_any(dp, dt, r * cols + c) * ld_any(p, dt, r * cols + c);
-  const float rd = warp_sum(s);
-  for (int64_t c = lane; c < cols; c += 32) {
-    const int64_t o = r * cols + c;
-    const float pv = ld_any(p, dt, o);
-    st_any(dp, dt, o, pv * (ld_any(dp, dt, o) - rd) * scale);
-  }
-}
-
 __global__ void copy_heads_kernel(const void* src, int64_t src_ld, int64_t src_hs, void* dst,
                                   int64_t dst_ld, int64_t dst_hs, int64_t rows, int64_t heads,
                                   int64_t dh, int dt) {
@@ -368,46 +277,6 @@ void k_ln_bwd_dx(const void* dy, int dt, const void* xhat, int xdt, const float*
   ln_bwd_dx_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dy, dt, xhat, xdt, gamma, inv_std, rs,
                                                          inv_h, rows, cols, resid, rdt, dx, dxdt);
   check_launch("ln_bwd_dx");
-}
-
-void k_softmax_rowmax(const void* sc, int dt, int64_t rows, int64_t cols, float* mx,
-                      cudaStream_t s) {
-  softmax_rowmax_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(sc, dt, rows, cols, mx);
-  check_launch("softmax_rowmax");
-}
-void k_softmax_rowexpsum(const void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
-                         float* sum, cudaStream_t s) {
-  softmax_rowexpsum_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(sc, dt, rows, cols,
-                                                                            mx, sum);
-  check_launch("softmax_rowexpsum");
-}
-void k_softmax_norm(void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
-                    const float* sum, cudaStream_t s) {
-  softmax_norm_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(sc, dt, rows, cols, mx,
-                                                                       sum);
-  check_launch("softmax_norm");
-}
-void k_softmax_fused(void* sc, int dt, int64_t rows, int64_t cols, cudaStream_t s) {
-  softmax_fused_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(sc, dt, rows, cols);
-  check_launch("softmax_fused");
-}
-void k_softmax_bwd_rowdot(const void* dp, const void* p, int dt, int64_t rows, int64_t cols,
-                          float* rowdot, cudaStream_t s) {
-  softmax_bwd_rowdot_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(dp, p, dt, rows,
-                                                                             cols, rowdot);
-  check_launch("softmax_bwd_rowdot");
-}
-void k_softmax_bwd_ds(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
-                      const float* rowdot, float scale, cudaStream_t s) {
-  softmax_bwd_ds_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dp, p, dt, rows, cols, rowdot,
-                                                              scale);
-  check_launch("softmax_bwd_ds");
-}
-void k_softmax_bwd_fused(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
-                         float scale, cudaStream_t s) {
-  softmax_bwd_fused_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(dp, p, dt, rows,
-                                                                            cols, scale);
-  check_launch("softmax_bwd_fused");
 }
 
 void k_copy_heads(const void* src, int64_t src_ld, int64_t src_hs, void* dst, int64_t dst_ld,

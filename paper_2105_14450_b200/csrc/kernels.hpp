@@ -50,19 +50,21 @@ void k_ln_bwd_dx(const void* dy, int dt, const void* xhat, int xdt, const float*
                  const void* resid, int rdt, void* dx, int dxdt, cudaStream_t s);
 
 // ---- attention softmax (cube3d/attention.hpp:106-126, 161-169) ----
-void k_softmax_rowmax(const void* sc, int dt, int64_t rows, int64_t cols, float* mx,
-                      cudaStream_t s);
-void k_softmax_rowexpsum(const void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
+// Scores / dP are fp32 (bf16 logits would distort exp after LayerNorm); the
+// probabilities P and dS are written in the activation dtype for the GEMMs.
+void k_softmax_rowmax(const float* sc, int64_t rows, int64_t cols, float* mx, cudaStream_t s);
+void k_softmax_rowexpsum(const float* sc, int64_t rows, int64_t cols, const float* mx,
                          float* sum, cudaStream_t s);
-void k_softmax_norm(void* sc, int dt, int64_t rows, int64_t cols, const float* mx,
-                    const float* sum, cudaStream_t s);
-void k_softmax_fused(void* sc, int dt, int64_t rows, int64_t cols, cudaStream_t s);
-void k_softmax_bwd_rowdot(const void* dp, const void* p, int dt, int64_t rows, int64_t cols,
+void k_softmax_norm(const float* sc, int64_t rows, int64_t cols, const float* mx,
+                    const float* sum, void* p, int pdt, cudaStream_t s);
+void k_softmax_fused(const float* sc, int64_t rows, int64_t cols, void* p, int pdt,
+                     cudaStream_t s);
+void k_softmax_bwd_rowdot(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                           float* rowdot, cudaStream_t s);
-void k_softmax_bwd_ds(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
-                      const float* rowdot, float scale, cudaStream_t s);
-void k_softmax_bwd_fused(void* dp, const void* p, int dt, int64_t rows, int64_t cols,
-                         float scale, cudaStream_t s);
+void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
+                      const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s);
+void k_softmax_bwd_fused(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
+                         float scale, void* ds, int dsdt, cudaStream_t s);
 
 // dst[r][h*dst_hs + t] = src[r][h*src_hs + t], t < dh (head-major column blocks).
 void k_copy_heads(const void* src, int64_t src_ld, int64_t src_hs, void* dst, int64_t dst_ld,

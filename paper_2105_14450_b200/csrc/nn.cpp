@@ -314,27 +314,29 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
   } else {
     qv = qkv_view(qkv.data, dt, a, 0, false);
   }
-  // scores = scale * Q K^T  ([slice][S][sl])
-  DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(nslices * a.S * a.sl) * dtype_size(dt), s));
+  // scores = scale * Q K^T  ([slice][S][sl], fp32)
+  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
+  DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s));
   S.probs = pb.get();
   {
+    DevBuf sc(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
-    e.out = scores_view(pb.get(), dt, a, false);
+    e.out = scores_view(sc.get(), kF32, a, false);
     e.alpha = a.scale;
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, qv, qkv_view(qkv.data, dt, a, 1, false), e, s);
-  }
-  // distributed softmax over the key blocks of the seq axis
-  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
-  if (a.Ps == 1) {
-    k_softmax_fused(pb.get(), dt, srows, a.sl, s);
-  } else {
-    DevBuf mx(static_cast<size_t>(srows) * sizeof(float), s);
-    DevBuf sm(static_cast<size_t>(srows) * sizeof(float), s);
-    k_softmax_rowmax(pb.get(), dt, srows, a.sl, mx.as<float>(), s);
-    cube.all_reduce(a.seq_axis, mx.get(), srows, kF32, true, s);
-    k_softmax_rowexpsum(pb.get(), dt, srows, a.sl, mx.as<float>(), sm.as<float>(), s);
-    cube.all_reduce(a.seq_axis, sm.get(), srows, kF32, false, s);
-    k_softmax_norm(pb.get(), dt, srows, a.sl, mx.as<float>(), sm.as<float>(), s);
+    // distributed softmax over the key blocks of the seq axis
+    const float* scf = sc.as<float>();
+    if (a.Ps == 1) {
+      k_softmax_fused(scf, srows, a.sl, pb.get(), dt, s);
+    } else {
+      DevBuf mx(static_cast<size_t>(srows) * sizeof(float), s);
+      DevBuf sm(static_cast<size_t>(srows) * sizeof(float), s);
+      k_softmax_rowmax(scf, srows, a.sl, mx.as<float>(), s);
+      cube.all_reduce(a.seq_axis, mx.get(), srows, kF32, true, s);
+      k_softmax_rowexpsum(scf, srows, a.sl, mx.as<float>(), sm.as<float>(), s);
+      cube.all_reduce(a.seq_axis, sm.get(), srows, kF32, false, s);
+      k_softmax_norm(scf, srows, a.sl, mx.as<float>(), sm.as<float>(), pb.get(), dt, s);
+    }
   }
   // context = P V, reduce-scattered back to this rank's seq block
   const ActGeom cg = act_geom(cube.grid(), x.batch, x.seq, cfg.hidden, qkv.group);
@@ -376,11 +378,12 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
 
   Gathered dcf = gather(cube, a.seq_axis, dctx.data, rows * a.hd, dt, s);
   DevBuf dqkv_buf(static_cast<size_t>(rows * a.ld_qkv) * dtype_size(dt), s);
-  // dP = dctx_full V^T
-  DevBuf dp(static_cast<size_t>(nslices * a.S * a.sl) * dtype_size(dt), s);
+  // dP = dctx_full V^T (fp32)
+  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
+  DevBuf dpf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
   {
     Epilogue e;
-    e.out = scores_view(dp.get(), dt, a, false);
+    e.out = scores_view(dpf.get(), kF32, a, false);
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
                qkv_view(qkv, dt, a, 2, false), e, s);
   }
@@ -392,14 +395,15 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                packed_view(dcf.ptr, dt, a, true), e, s);
   }
   // dS = P * (dP - rowdot) * scale, rowdot summed along the seq axis
-  const int64_t srows = static_cast<int64_t>(nslices) * a.S;
+  DevBuf dp(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s);  // dS, activation dtype
   if (a.Ps == 1) {
-    k_softmax_bwd_fused(dp.get(), S.probs, dt, srows, a.sl, a.scale, s);
+    k_softmax_bwd_fused(dpf.as<float>(), S.probs, dt, srows, a.sl, a.scale, dp.get(), dt, s);
   } else {
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
-    k_softmax_bwd_rowdot(dp.get(), S.probs, dt, srows, a.sl, rd.as<float>(), s);
+    k_softmax_bwd_rowdot(dpf.as<float>(), S.probs, dt, srows, a.sl, rd.as<float>(), s);
     cube.all_reduce(a.seq_axis, rd.get(), srows, kF32, false, s);
-    k_softmax_bwd_ds(dp.get(), S.probs, dt, srows, a.sl, rd.as<float>(), a.scale, s);
+    k_softmax_bwd_ds(dpf.as<float>(), S.probs, dt, srows, a.sl, rd.as<float>(), a.scale,
+                     dp.get(), dt, s);
   }
   // dQ = dS K (reduce-scattered), dK = dS^T Q_full
   {

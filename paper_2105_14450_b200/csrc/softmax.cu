@@ -1,0 +1,143 @@
+// Distributed attention softmax (cube3d/attention.hpp:106-126) and its adjoint
+// (:161-169), batched over every local (batch, head) slice: one warp per score row.
+// Scores and dP arrive in fp32; P and dS leave in the activation dtype.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "epi.cuh"
+#include "kernels.hpp"
+
+namespace c3d {
+
+namespace {
+
+constexpr int kWarps = 8;
+
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float wmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+inline unsigned blocks_for(int64_t rows) { return static_cast<unsigned>((rows + kWarps - 1) / kWarps); }
+
+#define ROW_PROLOGUE                                                                   \
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarps) + threadIdx.x / 32;      \
+  const int lane = threadIdx.x % 32;                                                   \
+  if (r >= rows) return;                                                               \
+  const float* srow = sc + r * cols;
+
+__global__ void rowmax_kernel(const float* sc, int64_t rows, int64_t cols, float* mx) {
+  ROW_PROLOGUE
+  float m = -INFINITY;
+  for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, srow[c]);
+  m = wmax(m);
+  if (lane == 0) mx[r] = m;
+}
+
+__global__ void rowexpsum_kernel(const float* sc, int64_t rows, int64_t cols, const float* mx,
+                                 float* sum) {
+  ROW_PROLOGUE
+  const float m = mx[r];
+  float s = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) s += expf(srow[c] - m);
+  s = wsum(s);
+  if (lane == 0) sum[r] = s;
+}
+
+__global__ void norm_kernel(const float* sc, int64_t rows, int64_t cols, const float* mx,
+                            const float* sum, void* p, int pdt) {
+  ROW_PROLOGUE
+  const float m = mx[r], inv = 1.f / sum[r];
+  for (int64_t c = lane; c < cols; c += 32) st_any(p, pdt, r * cols + c, expf(srow[c] - m) * inv);
+}
+
+__global__ void fused_kernel(const float* sc, int64_t rows, int64_t cols, void* p, int pdt) {
+  ROW_PROLOGUE
+  float m = -INFINITY;
+  for (int64_t c = lane; c < cols; c += 32) m = fmaxf(m, srow[c]);
+  m = wmax(m);
+  float s = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) s += expf(srow[c] - m);
+  const float inv = 1.f / wsum(s);
+  for (int64_t c = lane; c < cols; c += 32) st_any(p, pdt, r * cols + c, expf(srow[c] - m) * inv);
+}
+
+__global__ void bwd_rowdot_kernel(const float* sc, const void* p, int pdt, int64_t rows,
+                                  int64_t cols, float* rowdot) {
+  ROW_PROLOGUE
+  float s = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) s += srow[c] * ld_any(p, pdt, r * cols + c);
+  s = wsum(s);
+  if (lane == 0) rowdot[r] = s;
+}
+
+__global__ void bwd_ds_kernel(const float* sc, const void* p, int pdt, int64_t rows,
+                              int64_t cols, const float* rowdot, float scale, void* ds,
+                              int dsdt) {
+  ROW_PROLOGUE
+  const float rd = rowdot[r];
+  for (int64_t c = lane; c < cols; c += 32) {
+    const float pv = ld_any(p, pdt, r * cols + c);
+    st_any(ds, dsdt, r * cols + c, pv * (srow[c] - rd) * scale);
+  }
+}
+
+__global__ void bwd_fused_kernel(const float* sc, const void* p, int pdt, int64_t rows,
+                                 int64_t cols, float scale, void* ds, int dsdt) {
+  ROW_PROLOGUE
+  float s = 0.f;
+  for (int64_t c = lane; c < cols; c += 32) s += srow[c] * ld_any(p, pdt, r * cols + c);
+  const float rd = wsum(s);
+  for (int64_t c = lane; c < cols; c += 32) {
+    const float pv = ld_any(p, pdt, r * cols + c);
+    st_any(ds, dsdt, r * cols + c, pv * (srow[c] - rd) * scale);
+  }
+}
+
+#undef ROW_PROLOGUE
+
+}  // namespace
+
+#define LAUNCH_ROWS(kern, name, ...)                                               \
+  do {                                                                             \
+    if (rows == 0) return;                                                         \
+    kern<<<blocks_for(rows), 32 * kWarps, 0, s>>>(__VA_ARGS__);                    \
+    check_launch(name);                                                            \
+  } while (0)
+
+void k_softmax_rowmax(const float* sc, int64_t rows, int64_t cols, float* mx, cudaStream_t s) {
+  LAUNCH_ROWS(rowmax_kernel, "softmax_rowmax", sc, rows, cols, mx);
+}
+void k_softmax_rowexpsum(const float* sc, int64_t rows, int64_t cols, const float* mx,
+                         float* sum, cudaStream_t s) {
+  LAUNCH_ROWS(rowexpsum_kernel, "softmax_rowexpsum", sc, rows, cols, mx, sum);
+}
+void k_softmax_norm(const float* sc, int64_t rows, int64_t cols, const float* mx,
+                    const float* sum, void* p, int pdt, cudaStream_t s) {
+  LAUNCH_ROWS(norm_kernel, "softmax_norm", sc, rows, cols, mx, sum, p, pdt);
+}
+void k_softmax_fused(const float* sc, int64_t rows, int64_t cols, void* p, int pdt,
+                     cudaStream_t s) {
+  LAUNCH_ROWS(fused_kernel, "softmax_fused", sc, rows, cols, p, pdt);
+}
+void k_softmax_bwd_rowdot(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
+                          float* rowdot, cudaStream_t s) {
+  LAUNCH_ROWS(bwd_rowdot_kernel, "softmax_bwd_rowdot", dp, p, pdt, rows, cols, rowdot);
+}
+void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
+                      const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s) {
+  LAUNCH_ROWS(bwd_ds_kernel, "softmax_bwd_ds", dp, p, pdt, rows, cols, rowdot, scale, ds, dsdt);
+}
+void k_softmax_bwd_fused(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
+                         float scale, void* ds, int dsdt, cudaStream_t s) {
+  LAUNCH_ROWS(bwd_fused_kernel, "softmax_bwd_fused", dp, p, pdt, rows, cols, scale, ds, dsdt);
+}
+
+}  // namespace c3d

@@ -1,0 +1,130 @@
+"""Transformer layer fwd+bwd on one B200 against the reference's golden outputs
+(run_layer through its 3-D path, tests/golden/layer_*.npz) and the pinned oracle.
+
+fp32 mode: every output and gradient within 1e-5 norm-wise of the fp64 reference.
+bf16 tensor-core mode: within 2e-2 norm-wise (and 5e-2 on the reference's max-rel
+metric) of the fp64 oracle evaluated on the same bf16-rounded inputs and parameters."""
+import numpy as np
+import pytest
+
+from oracle import cube3d_oracle as O
+from paper_2105_14450_b200 import C3DError, cube3d as c3
+
+from helpers import (TOL_F32_NORM, bf16_round, check_bf16, global_params_from, golden,
+                     map_params, oracle_params, to_np)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cube(torch_cuda):
+    c = c3.Cube((1, 1, 1), 0, 0)
+    yield c
+    c.close()
+
+
+def run_layer(cube, gp, x, dy, b, s, n, h, dtype, mode):
+    import torch
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params = c3.partition_layer_params(cube, gp, 0, dtype)
+    X = c3.activation_to_device(cube, x, b, s, 0, dtype)
+    DY = c3.activation_to_device(cube, dy, b, s, 0, dtype)
+    gs = c3.GroupState(0)
+    y, saved = c3.transformer_layer_fwd(cube, X, params, cfg, gs, mode)
+    assert gs.input_group == 0  # the layer preserves the group index
+    dx, grads = c3.transformer_layer_bwd(cube, DY, saved, params, cfg, mode, grad_dtype=c3.F32)
+    torch.cuda.synchronize()
+    gr = {f: to_np(getattr(grads, f).shard) for f in O.FIELDS}
+    return to_np(y.local), to_np(dx.local), gr
+
+
+@pytest.mark.parametrize("name", ["layer_toy", "layer_small"])
+def test_layer_fp32_vs_reference_golden(cube, name):
+    d = golden(name)
+    _, b, s, n, h, _ = (int(v) for v in d["cfg"])
+    gp = global_params_from(d)
+    y, dx, gr = run_layer(cube, gp, d["x"], d["dy"], b, s, n, h, c3.F32, c3.MODE_F32)
+    assert O.normwise_err(y, d["y"]) < TOL_F32_NORM
+    assert O.normwise_err(dx, d["dx"]) < TOL_F32_NORM
+    for f in O.FIELDS:
+        want = d["g_" + f].reshape(gr[f].shape)
+        assert O.normwise_err(gr[f], want) < TOL_F32_NORM, f
+
+
+@pytest.mark.parametrize("name", ["layer_toy", "layer_small"])
+def test_layer_bf16_vs_reference_golden(cube, name):
+    d = golden(name)
+    _, b, s, n, h, _ = (int(v) for v in d["cfg"])
+    gp = map_params(global_params_from(d), bf16_round)
+    xb, dyb = bf16_round(d["x"]), bf16_round(d["dy"])
+    y, dx, gr = run_layer(cube, gp, xb, dyb, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    compare_bf16(y, dx, gr, gp, xb, dyb, b, s, n)
+
+
+def compare_bf16(y, dx, gr, gp, x, dy, b, s, n):
+    P = oracle_params(gp)
+    yo, cache = O.layer_fwd(x, P, b, s, n)
+    dxo, Go = O.layer_bwd(dy, cache, P, b, s, n)
+    ye, cache_e = O.layer_fwd(x, P, b, s, n, rnd=bf16_round)
+    dxe, Ge = O.layer_bwd(dy, cache_e, P, b, s, n, rnd=bf16_round)
+    check_bf16(y, yo, "y", ye)
+    check_bf16(dx, dxo, "dx", dxe)
+    for f in O.FIELDS:
+        shp = gr[f].shape
+        check_bf16(gr[f], getattr(Go, f).reshape(shp), f, getattr(Ge, f).reshape(shp))
+
+
+@pytest.mark.parametrize("shape", [(4, 128, 4, 256), (2, 512, 16, 1024)])
+def test_layer_bf16_tensor_core_shapes(cube, shape):
+    """Shapes where every GEMM takes the tcgen05 path (dh = 64), vs the oracle."""
+    b, s, n, h = shape
+    r = O.Rng(99)
+    P = O.init_layer_params(h, 99)
+    gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
+    x = bf16_round(O.random_matrix(b * s, h, r))
+    dy = bf16_round(O.random_matrix(b * s, h, r))
+    launches0 = c3.launch_count()
+    y, dx, gr = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    assert c3.launch_count() > launches0
+    compare_bf16(y, dx, gr, gp, x, dy, b, s, n)
+
+
+def test_layer_fp32_mid_shape(cube):
+    b, s, n, h = 2, 64, 4, 128
+    r = O.Rng(3)
+    P = O.init_layer_params(h, 3)
+    gp = c3.GlobalLayerParams(**{f: getattr(P, f) for f in O.FIELDS})
+    x = O.random_matrix(b * s, h, r)
+    dy = O.random_matrix(b * s, h, r)
+    y, dx, gr = run_layer(cube, gp, x, dy, b, s, n, h, c3.F32, c3.MODE_F32)
+    yo, cache = O.layer_fwd(x, P, b, s, n)
+    dxo, Go = O.layer_bwd(dy, cache, P, b, s, n)
+    assert O.normwise_err(y, yo) < TOL_F32_NORM
+    assert O.normwise_err(dx, dxo) < TOL_F32_NORM
+    for f in O.FIELDS:
+        assert O.normwise_err(gr[f], getattr(Go, f).reshape(gr[f].shape)) < TOL_F32_NORM, f
+
+
+def test_layer_run_determinism(cube):
+    """Repeated runs are bitwise identical (cube3d/verify.hpp:738-744)."""
+    d = golden("layer_small")
+    _, b, s, n, h, _ = (int(v) for v in d["cfg"])
+    gp = map_params(global_params_from(d), bf16_round)
+    r1 = run_layer(cube, gp, d["x"], d["dy"], b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    r2 = run_layer(cube, gp, d["x"], d["dy"], b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+    assert all(np.array_equal(r1[2][f], r2[2][f]) for f in O.FIELDS)
+
+
+def test_layer_config_errors(cube):
+    gp = c3.init_layer_params(c3.TransformerConfig(2, 8, 3, 16), 1)
+    params = c3.partition_layer_params(cube, gp, 0, c3.F32)
+    X = c3.activation_to_device(cube, np.zeros((16, 16)), 2, 8, 0, c3.F32)
+    with pytest.raises(C3DError) as e:  # hidden % heads != 0
+        c3.transformer_layer_fwd(cube, X, params, c3.TransformerConfig(2, 8, 3, 16),
+                                 c3.GroupState(0))
+    assert e.value.name == "ConfigInvalid"
+    with pytest.raises(C3DError) as e:
+        c3.transformer_layer_fwd(cube, X, params, c3.TransformerConfig(2, 8, 2, 16),
+                                 c3.GroupState(1))
+    assert e.value.name == "GroupMismatch"
