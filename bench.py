@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: 3-D parallel Transformer layer fwd+bwd on 1/2/4/8 B200s.
+
+Workload (default, BASELINE.json configs[2], the north star's target): one
+3-D-partitioned Transformer layer, BERT-large shape (batch 32, seq 512, 16 heads,
+hidden 1024), forward + backward, bf16 storage / tcgen05 bf16 GEMMs with fp32
+accumulation. Grids: 1 GPU -> 1x1x1, 2 -> 2x1x1, 4 -> 1x2x2, 8 -> 2x2x2 cube; the
+global problem is fixed (strong scaling). Synthetic random inputs and weights.
+
+    python bench.py [--gpus N --steps K --warmup W]          # our arm
+    python bench.py --impl reference [...]                  # reference CPU arm
+    torchrun --nproc-per-node N bench.py --gpus N ...        # N > 1
+
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import signal
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "cfg3": dict(b=32, s=512, n=16, h=1024,
+                 desc="one 3-D Transformer layer fwd+bwd, BERT-large shape (b=32, s=512, "
+                      "16 heads, hidden 1024)"),
+    "cfg3-small": dict(b=8, s=512, n=16, h=1024, desc="cfg3 shape at batch 8"),
+}
+METRIC = "transformer_layer_fwd_bwd_seq_per_s"
+UNIT = "seq/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.send_signal(signal.SIGTERM)
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("bf16_tflops_sustained", 1400.2), d.get("hbm_gbs", 6552.3), "measured"
+    return 1400.0, 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- CPU reference
+def cpu_reference_sample(wl, p_ref=2, batch=2, seed=7):
+    """The reference's own CPU implementation (oracle/_ref: run_layer through its 3-D
+    path on a p=2 cube, one std::thread per rank) on a bounded batch of the workload.
+    Falls back to the numpy oracle port when the reference library was not built."""
+    import numpy as np
+    from oracle import ref
+    s, n, h = wl["s"], wl["n"], wl["h"]
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (batch * s, h))
+    dy = rng.uniform(-1, 1, (batch * s, h))
+    if ref.available():
+        params = ref.init_layer_params(h, seed)
+        t0 = time.perf_counter()
+        ref.run_layer(p_ref, batch, s, n, h, params, x, dy, f32=True)
+        dt = time.perf_counter() - t0
+        return dt, dict(kind="reference", cores=p_ref ** 3,
+                        sample=f"reference run_layer<float> fwd+bwd, p={p_ref} cube "
+                               f"({p_ref ** 3} rank threads), batch {batch} of the "
+                               f"workload shape (s={s}, n={n}, h={h})")
+    from oracle import cube3d_oracle as O
+    P = O.init_layer_params(h, seed)
+    t0 = time.perf_counter()
+    y, c = O.layer_fwd(x, P, batch, s, n)
+    O.layer_bwd(dy, c, P, batch, s, n)
+    dt = time.perf_counter() - t0
+    return dt, dict(kind="port", cores=os.cpu_count() or 1,
+                    sample=f"numpy oracle port fwd+bwd, batch {batch} (s={s}, n={n}, h={h})")
+
+
+def reference_arm(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    batch = 2
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_sample(wl, batch=batch)
+    times = []
+    meta = None
+    for _ in range(args.steps):
+        dt, meta = cpu_reference_sample(wl, batch=batch)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = batch / t
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["desc"], "global_batch": wl["b"], "seq_len": wl["s"],
+                   "hidden": wl["h"], "heads": wl["n"], "sample_batch": batch},
+        "cpu_baseline": {"value": value, "unit": UNIT, **meta},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------------- our arm
+def make_layer_inputs(cube, wl, dtype):
+    import torch
+    from paper_2105_14450_b200 import cube3d as c3
+    b, s, n, h = wl["b"], wl["s"], wl["n"], wl["h"]
+    dev = cube.device_str()
+    gen = torch.Generator(device=dev).manual_seed(1234 + cube.rank)
+    tdt = c3.torch_dtype(dtype)
+
+    def mat(rows, cols, dirs):
+        shp = cube.local_shape(c3.WEIGHT, rows, cols, dirs)
+        t = (torch.rand(shp, device=dev, generator=gen) * 0.2 - 0.1).to(tdt)
+        return c3.ShardedMatrix(t, rows, cols, c3.WEIGHT, dirs)
+
+    def vec(nn, one=False):
+        t = torch.rand((cube.diag_len(nn),), device=dev, generator=gen) * 0.2 - 0.1
+        return c3.DiagonalVector(t + 1.0 if one else t, nn)
+
+    d0, d1 = c3.triple_for_group(0), c3.triple_for_group(1)
+    params = c3.LayerParams(vec(h, True), vec(h), mat(h, 3 * h, d0), vec(3 * h), mat(h, h, d1),
+                            vec(h), vec(h, True), vec(h), mat(h, 4 * h, d0), vec(4 * h),
+                            mat(4 * h, h, d1), vec(h))
+    shp = cube.act_shape(b, s, h, 0)
+    x = c3.Activation3D((torch.rand(shp, device=dev, generator=gen) * 2 - 1).to(tdt), b, s, h, 0)
+    dy = c3.Activation3D((torch.rand(shp, device=dev, generator=gen) * 2 - 1).to(tdt), b, s, h, 0)
+    return params, x, dy
+
+
+def our_arm(args, wl):
+    import torch
+    from paper_2105_14450_b200 import cube3d as c3
+    from paper_2105_14450_b200 import dist
+    rank, world, local = dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}")
+    cube = dist.make_cube()
+    b, s, n, h = wl["b"], wl["s"], wl["n"], wl["h"]
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params, x, dy = make_layer_inputs(cube, wl, c3.BF16)
+    grads = c3.empty_like_params(cube, params, c3.F32)
+    stream = torch.cuda.current_stream()
+
+    def step(xa, dya):
+        gs = c3.GroupState(0)
+        y, saved = c3.transformer_layer_fwd(cube, xa, params, cfg, gs)
+        dx, _ = c3.transformer_layer_bwd(cube, dya, saved, params, cfg, grads=grads)
+        return y, dx
+
+    for _ in range(max(args.warmup, 3)):
+        step(x, dy)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    c3.prof_enable(True)
+    l0 = c3.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(x, dy)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = c3.launch_count() - l0
+    gemm_ms, gemm_flops, gemm_n = c3.prof_read()
+    c3.prof_enable(False)
+    clk = clocks.stop()
+    dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_max = dist.max_over_ranks(ms)
+    value = b / (ms_max * 1e-3)
+
+    # ---- end-to-end through the public API with host buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        xh = x.local.cpu().pin_memory()
+        dyh = dy.local.cpu().pin_memory()
+        dxh = torch.empty(x.local.shape, dtype=x.local.dtype, pin_memory=True)
+        xd = c3.Activation3D(torch.empty_like(x.local), b, s, h, 0)
+        dyd = c3.Activation3D(torch.empty_like(dy.local), b, s, h, 0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            xd.local.copy_(xh, non_blocking=True)
+            dyd.local.copy_(dyh, non_blocking=True)
+            _, dx = step(xd, dyd)
+            dxh.copy_(dx.local, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = dist.max_over_ranks(f0.elapsed_time(f1) / args.steps)
+        nbytes = x.local.numel() * x.local.element_size()
+        e2e = {"value": b / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 2 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
+               "path": "cube3d.transformer_layer_fwd/bwd over the C ABI, pinned host x/dy in, "
+                       "dx out, per step"}
+
+    # ---- roofline of the dominant kernel (tcgen05 GEMM), live per-launch timing
+    peak_tc, peak_hbm, peak_src = measured_peaks()
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    traffic = None
+    tp = ROOT / "profiles" / "gemm_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    # layer-level algorithmic flops (reference cost model, cube3d/cost_model.hpp:195-208)
+    from oracle.cube3d_oracle import layer_madds
+    mf, mb = layer_madds(b, s, n, h, 1)
+    layer_flops = 2.0 * (mf + mb)
+    layer_tflops = layer_flops / (ms_max * 1e-3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            dt, meta = cpu_reference_sample(wl)
+            cpu = {"value": 2 / dt, "unit": UNIT, **meta}
+        except Exception as ex:  # report, never fake
+            cpu = {"value": None, "unit": UNIT, "error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": wl["desc"], "grid": "x".join(map(str, cube.dims)),
+                       "global_batch": b, "seq_len": s, "hidden": h, "heads": n,
+                       "parallelism": f"3d-tensor-parallel px*py*pz={'x'.join(map(str, cube.dims))}",
+                       "l2": "per-step working set (weights, activations, saved state, "
+                             "scores) > 1 GB, larger than the 126 MB L2"},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": {"bound": "tensor", "kernel": "tc_gemm (tcgen05 + TMA, bf16->fp32)",
+                         "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
+                         "frac": achieved / peak_tc if peak_tc else None, "traffic": traffic,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "launches": gemm_n, "kernel_ms_per_step": gemm_ms / args.steps,
+                         "share_of_step": (gemm_ms / args.steps) / ms},
+            "layer_tflops": layer_tflops,
+            "layer_frac_of_peak": layer_tflops / (peak_tc * world),
+            "clocks": clk,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    cube.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+    return our_arm(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

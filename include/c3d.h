@@ -85,6 +85,11 @@ const char* c3d_last_error(void);
 const char* c3d_version(void);
 /* Number of kernels this library has launched in this process. */
 long long c3d_launch_count(void);
+/* Live kernel timing: when enabled, every tcgen05 GEMM launch is bracketed by CUDA
+ * events on its own stream; c3d_prof_read returns the summed per-launch time (ms),
+ * summed algorithmic flops (2*M*N*K*batch) and launch count, then resets. */
+int c3d_prof_enable(int on);
+int c3d_prof_read(double* ms, double* flops, long long* launches);
 
 /* ------------------------------------------------------ pure host: inputs */
 /* Rng (cube3d/rng.hpp:17-34): mt19937_64 with the reference's explicit 53-bit

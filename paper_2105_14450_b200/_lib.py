@@ -81,6 +81,8 @@ SIGNATURES = {
     "c3d_last_error": [],
     "c3d_version": [],
     "c3d_launch_count": [],
+    "c3d_prof_enable": [C.c_int],
+    "c3d_prof_read": [P(C.c_double), P(C.c_double), P(C.c_longlong)],
     "c3d_rng_create": [C.c_uint64, P(VP)],
     "c3d_rng_destroy": [VP],
     "c3d_rng_next_u64": [VP, P(C.c_uint64), C.c_int64],

@@ -178,6 +178,12 @@ extern "C" {
 const char* c3d_last_error(void) { return g_last_error.c_str(); }
 const char* c3d_version(void) { return "c3d-b200 0.1 (sm_100a)"; }
 long long c3d_launch_count(void) { return c3d::launch_counter().load(); }
+int c3d_prof_enable(int on) {
+  return guard([&] { c3d::prof_enable(on != 0); });
+}
+int c3d_prof_read(double* ms, double* flops, long long* launches) {
+  return guard([&] { c3d::prof_read(ms, flops, launches); });
+}
 
 // ---------------------------------------------------------------- rng
 int c3d_rng_create(uint64_t seed, c3d_rng** out) {

@@ -1,6 +1,8 @@
 #include "cube.hpp"
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 namespace c3d {
 
@@ -54,7 +56,26 @@ ncclComm_t Cube::comm(int axis) const {
   return axis_comm_[axis];
 }
 
+namespace {
+bool trace_on() {
+  static const bool on = std::getenv("C3D_TRACE") != nullptr;
+  return on;
+}
+}  // namespace
+
 void Cube::charge(int kind, uint64_t sent, uint64_t received) {
+  if (trace_on()) {
+    static const char* names[] = {"broadcast", "all_gather", "reduce_scatter", "all_reduce",
+                                  "barrier"};
+    std::fprintf(stderr, "[c3d rank %d] #%llu %s sent=%llu recv=%llu\n", rank_,
+                 static_cast<unsigned long long>(counters_.calls_by_kind[0] +
+                                                 counters_.calls_by_kind[1] +
+                                                 counters_.calls_by_kind[2] +
+                                                 counters_.calls_by_kind[3]),
+                 names[kind], static_cast<unsigned long long>(sent),
+                 static_cast<unsigned long long>(received));
+    std::fflush(stderr);
+  }
   counters_.elements_sent += sent;
   counters_.elements_received += received;
   counters_.sent_by_kind[kind] += sent;

@@ -121,7 +121,9 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
   Mat dyf = flatten(cube, dy);
   if (dyf.dirs != saved.x.dirs.swapped())
     fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB backward must carry the swapped triple");
-  if (db && db->data) {
+  // The reduction is collective: every rank joins it whether or not it holds a
+  // diagonal slice (non-holders pass a vector with no local data).
+  if (db) {
     DevBuf cs(static_cast<size_t>(dyf.cols) * sizeof(float), s);
     k_colsum(dyf.data, dyf.dtype, nullptr, kF32, dyf.rows, dyf.cols, cs.as<float>(), s);
     Vec out = *db;
@@ -184,7 +186,7 @@ void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const 
     fail(C3D_ERR_SHAPE_MISMATCH, "layer norm gradient does not match the saved forward");
   const Dirs d = triple_for_group(dy.group);
   const float inv_h = 1.f / static_cast<float>(dy.hidden);
-  if (dgamma && dbeta && dgamma->data && dbeta->data) {
+  if (dgamma && dbeta) {  // collective on every rank (see linear_bwd)
     DevBuf cs(static_cast<size_t>(2 * dy.cols) * sizeof(float), s);
     k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, cs.as<float>(), s);
     k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, cs.as<float>() + dy.cols, s);

@@ -13,6 +13,8 @@
 namespace c3d {
 
 void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s);
+void prof_enable(bool on);
+void prof_read(double* ms, double* flops, long long* launches);
 
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,

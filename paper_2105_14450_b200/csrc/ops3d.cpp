@@ -161,6 +161,9 @@ void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nve
   const int px = g.dims[kX];
   const int64_t block = n2 * px;  // per-vector column-sum length (len / p_out)
   const bool holder = diagonal_holder(cube.coords());
+  for (int k = 0; k < nvec; ++k)
+    if (holder && outs[k].data == nullptr)
+      fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
   if (g.size() == 1) {
     for (int k = 0; k < nvec; ++k) k_convert(colsums + k * block, kF32, outs[k].data, outs[k].dtype, n2, s);
     return;

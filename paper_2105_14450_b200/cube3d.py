@@ -846,3 +846,14 @@ def gemm(M, N, K, a_view: dict, b_view: dict, out_view: dict, alpha=1.0, bias=No
 
 def launch_count() -> int:
     return int(lib().c3d_launch_count())
+
+
+def prof_enable(on: bool = True) -> None:
+    call("c3d_prof_enable", int(on))
+
+
+def prof_read():
+    """-> (sum of tcgen05 GEMM launch times in ms, sum of their flops, launches)."""
+    ms, fl, n = C.c_double(), C.c_double(), C.c_longlong()
+    call("c3d_prof_read", C.byref(ms), C.byref(fl), C.byref(n))
+    return ms.value, fl.value, n.value

@@ -1,0 +1,25 @@
+"""Multi-GPU parity (2 GPUs -> 2x1x1, 4 GPUs -> 1x2x2): runs tools/mp_parity.py under
+torchrun, one rank per GPU. Skipped when the box has fewer GPUs."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_mp_parity(torch_cuda, n):
+    if torch_cuda.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + n),
+           str(ROOT / "tools" / "mp_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "PYTHONPATH": str(ROOT)})
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith(("PASS", "FAIL"))]
+    assert r.returncode == 0 and lines and all(ln.startswith("PASS") for ln in lines), (
+        r.stdout[-3000:] + r.stderr[-3000:])

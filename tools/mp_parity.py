@@ -1,0 +1,148 @@
+"""Multi-GPU parity driver (run under torchrun, one rank per GPU): 3-D matmuls and the
+Transformer layer on the grid for WORLD_SIZE, collected on rank 0 and compared with
+the reference's golden outputs / the pinned oracle. Prints PASS/FAIL lines; exit 1
+on failure. Used by tests/test_multigpu_gpu.py."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import cube3d_oracle as O  # noqa: E402
+from paper_2105_14450_b200 import cube3d as c3  # noqa: E402
+from paper_2105_14450_b200 import dist as cdist  # noqa: E402
+from helpers import bf16_round, golden, to_np  # noqa: E402
+
+FAILS = []
+
+
+def report(name, ok, detail=""):
+    if dist.get_rank() == 0:
+        print(("PASS " if ok else "FAIL ") + name + (f": {detail}" if detail else ""), flush=True)
+    if not ok:
+        FAILS.append(name)
+
+
+def gather_all(arr):
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, arr)
+    return out
+
+
+def matmul_checks(cube, dims):
+    q = dims[0] * dims[1] * dims[2]
+    n = 4 * q * q if q > 1 else 32
+    rng = O.Rng(500 + q)
+    a = O.random_integer_matrix(n, n, rng)
+    b = O.random_integer_matrix(n, n, rng)
+    g = O.random_integer_matrix(n, n, rng)
+    forms = {"AB": (c3.INPUT, c3.WEIGHT, c3.OUTPUT, None, c3.matmul_ab_fwd, c3.matmul_ab_bwd,
+                    a @ b, g @ b.T, a.T @ g),
+             "ABt": (c3.INPUT, c3.WEIGHT_OF_TRANSPOSE, c3.OUTPUT, None, c3.matmul_abt_fwd,
+                     c3.matmul_abt_bwd, a @ b.T, g @ b, g.T @ a),
+             "AtB": (c3.INPUT, c3.INPUT, c3.WEIGHT, c3.canonical_directions().swapped(),
+                     c3.matmul_atb_fwd, c3.matmul_atb_bwd, a.T @ b, b @ g.T, a @ g)}
+    for mode, dt in ((c3.MODE_F32, c3.F32), (c3.MODE_AUTO, c3.BF16)):
+        for form, (la, lb, lg, bd, fwd, bwd, wc, wda, wdb) in forms.items():
+            A = c3.shard_to_device(cube, a, la, dt)
+            B = c3.shard_to_device(cube, b, lb, dt, bd)
+            G = c3.shard_to_device(cube, g, lg, dt)
+            C = fwd(cube, A, B, mode, c3.F32)
+            dA, dB = bwd(cube, G, A, B, mode, c3.F32)
+            torch.cuda.synchronize()
+            res = []
+            for M, glob in ((C, wc), (dA, wda), (dB, wdb)):
+                fam = gather_all(to_np(M.shard))
+                got = c3.collect(fam, M.layout, dims, glob.shape[0], glob.shape[1], M.dirs)
+                res.append(np.array_equal(got, glob))
+            report(f"matmul-{form}-{'f32' if dt == c3.F32 else 'bf16'}-integer-bitwise", all(res),
+                   str(res))
+    if dims[1] != dims[2]:
+        return
+    # vector ops along the diagonal
+    vec = O.Rng(9).uniform(-1, 1, n)
+    am = O.Rng(10).uniform(-1, 1, n * n).reshape(n, n)
+    A = c3.shard_to_device(cube, am, c3.INPUT, c3.F32)
+    V = c3.vector_to_device(cube, vec, c3.F32)
+    C = c3.add_vec_fwd(cube, A, V)
+    dA, db = c3.add_vec_bwd(cube, A)
+    torch.cuda.synchronize()
+    got = c3.collect(gather_all(to_np(C.shard)), c3.INPUT, dims, n, n)
+    gdb = c3.collect_diagonal(gather_all(to_np(db.shard)), dims, n)
+    report("add_vec-fwd-bwd", O.rel_err(got, am + vec) < 1e-6 and O.rel_err(gdb, am.sum(0)) < 1e-5)
+
+
+def layer_check(cube, dims, name, dtype, mode):
+    d = golden(name)
+    _, b, s, n, h, seed = (int(v) for v in d["cfg"])
+    gp = c3.GlobalLayerParams(**{f: np.array(d["p_" + f]) for f in O.FIELDS})
+    x, dy = d["x"], d["dy"]
+    if dtype == c3.BF16:
+        gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(gp, f)) for f in O.FIELDS})
+        x, dy = bf16_round(x), bf16_round(dy)
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params = c3.partition_layer_params(cube, gp, 0, dtype)
+    X = c3.activation_to_device(cube, x, b, s, 0, dtype)
+    DY = c3.activation_to_device(cube, dy, b, s, 0, dtype)
+    gs = c3.GroupState(0)
+    cube.reset_counters()
+    y, saved = c3.transformer_layer_fwd(cube, X, params, cfg, gs, mode)
+    dx, grads = c3.transformer_layer_bwd(cube, DY, saved, params, cfg, mode, grad_dtype=c3.F32)
+    torch.cuda.synchronize()
+    Y = c3.activation_to_global(gather_all(to_np(y.local)), b, s, h, 0, dims)
+    DX = c3.activation_to_global(gather_all(to_np(dx.local)), b, s, h, 0, dims)
+    G = {}
+    for f in O.FIELDS:
+        v = getattr(grads, f)
+        fam = gather_all(to_np(v.shard))
+        if f.startswith("w_"):
+            G[f] = c3.collect(fam, c3.WEIGHT, dims, v.global_rows, v.global_cols, v.dirs)
+        else:
+            G[f] = c3.collect_diagonal(fam, dims, v.global_len)
+    if dtype == c3.F32:
+        errs = {"y": O.normwise_err(Y, d["y"]), "dx": O.normwise_err(DX, d["dx"])}
+        for f in O.FIELDS:
+            errs[f] = O.normwise_err(G[f], d["g_" + f].reshape(G[f].shape))
+        ok = all(e < 1e-5 for e in errs.values())
+    else:
+        P = O.LayerParams(**{f: getattr(gp, f) for f in O.FIELDS})
+        yo, cache = O.layer_fwd(x, P, b, s, n)
+        dxo, Go = O.layer_bwd(dy, cache, P, b, s, n)
+        errs = {"y": O.normwise_err(Y, yo), "dx": O.normwise_err(DX, dxo)}
+        for f in O.FIELDS:
+            errs[f] = O.normwise_err(G[f], getattr(Go, f).reshape(G[f].shape))
+        ok = all(e < 2e-2 for e in errs.values())
+    worst = max(errs, key=errs.get)
+    report(f"layer-{name}-{'f32' if dtype == c3.F32 else 'bf16'}", ok,
+           f"worst {worst}={errs[worst]:.2e}")
+    # traffic: elements moved by all ranks (sent == received, cube3d/counters.hpp:32-36)
+    cnt = gather_all(cube.counters())
+    sent = sum(c["elements_sent"] for c in cnt)
+    recv = sum(c["elements_received"] for c in cnt)
+    report(f"layer-{name}-traffic-balanced", sent == recv, f"sent={sent} recv={recv}")
+
+
+def main():
+    rank, world, local = cdist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dims = c3.grid_for(world) if len(sys.argv) < 2 else tuple(int(v) for v in sys.argv[1].split("x"))
+    cube = cdist.make_cube(dims)
+    if os.environ.get("MP_SKIP_MATMUL") is None:
+        matmul_checks(cube, dims)
+    if dims[1] == dims[2]:
+        for name in ("layer_toy", "layer_small"):
+            layer_check(cube, dims, name, c3.F32, c3.MODE_F32)
+            layer_check(cube, dims, name, c3.BF16, c3.MODE_AUTO)
+    cube.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 1 if FAILS else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
