@@ -205,15 +205,53 @@ def our_arm(args, wl):
     grads = c3.empty_like_params(cube, params, c3.F32)
     stream = torch.cuda.current_stream()
 
+    outs = {}
+
     def step(xa, dya):
         gs = c3.GroupState(0)
         y, saved = c3.transformer_layer_fwd(cube, xa, params, cfg, gs)
         dx, _ = c3.transformer_layer_bwd(cube, dya, saved, params, cfg, grads=grads)
+        outs["y"], outs["dx"] = y, dx
         return y, dx
 
-    for _ in range(max(args.warmup, 3)):
+    # eager warm-up: at least W steps and ~1 s, so SM clocks leave their idle state
+    warm = 0
+    t0 = time.time()
+    while warm < max(args.warmup, 3) or time.time() - t0 < 1.0:
         step(x, dy)
+        warm += 1
+        if warm % 4 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
+    # eager (per-op launch) timing, for reference
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(x, dy)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_eager = dist.max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    # the whole fwd+bwd step as one CUDA graph (kernels, NCCL collectives and
+    # stream-ordered scratch allocations captured together)
+    graph = None
+    launches_per_step = None
+    if not args.no_graph:
+        dist.barrier()
+        l0 = c3.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(x, dy)
+        launches_per_step = c3.launch_count() - l0
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            step(x, dy)
 
     # ---- device-resident timed region
     dist.barrier()
@@ -221,22 +259,29 @@ def our_arm(args, wl):
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    c3.prof_enable(True)
     l0 = c3.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step(x, dy)
+        run_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    launches = c3.launch_count() - l0
-    gemm_ms, gemm_flops, gemm_n = c3.prof_read()
-    c3.prof_enable(False)
+    launches = (launches_per_step * args.steps if graph is not None
+                else c3.launch_count() - l0)
     clk = clocks.stop()
     dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     ms_max = dist.max_over_ranks(ms)
     value = b / (ms_max * 1e-3)
+
+    # ---- dominant-kernel (tcgen05 GEMM) timing: live per-launch CUDA events on the
+    # launching stream over K eager steps (events cannot sit inside the graph)
+    c3.prof_enable(True)
+    for _ in range(args.steps):
+        step(x, dy)
+    torch.cuda.synchronize()
+    gemm_ms, gemm_flops, gemm_n = c3.prof_read()
+    c3.prof_enable(False)
 
     # ---- end-to-end through the public API with host buffers (H2D + D2H inside)
     e2e = None
@@ -246,23 +291,39 @@ def our_arm(args, wl):
         dxh = torch.empty(x.local.shape, dtype=x.local.dtype, pin_memory=True)
         xd = c3.Activation3D(torch.empty_like(x.local), b, s, h, 0)
         dyd = c3.Activation3D(torch.empty_like(dy.local), b, s, h, 0)
+
+        def e2e_step():
+            xd.local.copy_(xh, non_blocking=True)
+            dyd.local.copy_(dyh, non_blocking=True)
+            _, dx = step(xd, dyd)
+            dxh.copy_(dx.local, non_blocking=True)
+
+        g2 = None
+        if not args.no_graph:
+            e2e_step()
+            torch.cuda.synchronize()
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2):
+                e2e_step()
+            for _ in range(3):
+                g2.replay()
         dist.barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.steps):
-            xd.local.copy_(xh, non_blocking=True)
-            dyd.local.copy_(dyh, non_blocking=True)
-            _, dx = step(xd, dyd)
-            dxh.copy_(dx.local, non_blocking=True)
+            if g2 is not None:
+                g2.replay()
+            else:
+                e2e_step()
         f1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = dist.max_over_ranks(f0.elapsed_time(f1) / args.steps)
         nbytes = x.local.numel() * x.local.element_size()
         e2e = {"value": b / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 2 * nbytes * world, "d2h_bytes_per_step": nbytes * world,
-               "path": "cube3d.transformer_layer_fwd/bwd over the C ABI, pinned host x/dy in, "
-                       "dx out, per step"}
+               "path": "cube3d.transformer_layer_fwd/bwd over the C ABI (captured as one CUDA "
+                       "graph), pinned host x/dy copied in and dx copied out every step"}
 
     # ---- roofline of the dominant kernel (tcgen05 GEMM), live per-launch timing
     peak_tc, peak_hbm, peak_src = measured_peaks()
@@ -291,7 +352,8 @@ def our_arm(args, wl):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
+            "steps": args.steps, "warmup": warm, "ms_per_step": ms_max,
+            "ms_per_step_eager": ms_eager, "cuda_graph": graph is not None,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl["desc"], "grid": "x".join(map(str, cube.dims)),
@@ -306,7 +368,9 @@ def our_arm(args, wl):
                          "frac": achieved / peak_tc if peak_tc else None, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
                          "launches": gemm_n, "kernel_ms_per_step": gemm_ms / args.steps,
-                         "share_of_step": (gemm_ms / args.steps) / ms},
+                         "share_of_step": (gemm_ms / args.steps) / ms_eager,
+                         "timing": "per-launch CUDA events on the launching stream over "
+                                   f"{args.steps} eager steps"},
             "layer_tflops": layer_tflops,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
             "clocks": clk,
@@ -326,6 +390,7 @@ def main():
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

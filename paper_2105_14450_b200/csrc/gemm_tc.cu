@@ -5,25 +5,32 @@
 // `multiply_accumulate` (cube3d/matrix.hpp:68-92): the NN / NT / TN forms map to
 // K-major or MN-major UMMA operand descriptors instead of strided CPU loops.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer (one elected lane)           smem ring: full/empty mbarriers
-//   warp 1      TMEM allocator + UMMA issuer (one lane)   TMEM ring: 2 accumulators
-//   warps 2..5  epilogue: tcgen05.ld -> registers -> epilogue math -> st.global
-// Tile: 128 x BN (UMMA M=128, N=BN, K=16), K-block 64 per pipeline stage.
+// Structure (one CTA per SM, persistent over work units = output tiles x K splits):
+//   warp 0      TMA producer (one lane)                  smem ring: full/empty mbarriers
+//   warp 1      TMEM allocator + UMMA issuer (one lane)  TMEM ring: 2 accumulators
+//   warps 2..9  epilogue: tcgen05.ld -> registers -> epilogue math -> st.global
+//               (two warps per TMEM lane quarter, each owning half of the columns)
+// Tile: 128 x BN (UMMA M=128, N=BN, K=16), K-block 64 per pipeline stage. The
+// producer and issuer loops carry their stage/phase and TMA coordinates
+// incrementally: no integer division on the per-K-block path.
+// Split-K (batch 1 only): each split writes fp32 partials to a workspace and a
+// deterministic reduction kernel applies the epilogue.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
 #include <string>
 
+#include "common.hpp"
+#include "epi.cuh"
 #include "gemm.hpp"
 #include "gemm_tc.hpp"
-#include "epi.cuh"
 #include "ptx.cuh"
 
 namespace c3d {
@@ -32,7 +39,8 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kSmemBudget = 227 * 1024;
 
 struct TcOperand {
@@ -45,117 +53,168 @@ struct TcOperand {
 struct TcArgs {
   int M, N, K, batch;
   int m_tiles, n_tiles, k_blocks;
-  int num_tiles;
+  int num_tiles;  // output tiles (batch * m_tiles * n_tiles)
+  int ksplit, kb_per_split;
   int stages;
   int vec_ok;
+  float* ws;  // split-K partials [ksplit][M][N] fp32
   TcOperand a, b;
   Epilogue epi;
 };
 
-__device__ __forceinline__ void load_operand(const CUtensorMap* map, const TcOperand& op,
-                                             void* dst, uint64_t* bar, int r0, int rows,
-                                             int k0, int b) {
-  const int c3 = b % op.b_lo_n, c4 = b / op.b_lo_n;
+// TMA coordinates of one operand for the current tile, advanced per K-block.
+struct OpPos {
+  int r_lo[4];
+  int r_hi[4];
+  int k_lo, k_hi;
+  int c3, c4;
+};
+
+__device__ __forceinline__ void op_init(const TcOperand& op, OpPos& p, int r0, int nchunks, int k0,
+                                        int b) {
+  p.c3 = b % op.b_lo_n;
+  p.c4 = b / op.b_lo_n;
+  for (int j = 0; j < nchunks; ++j) {
+    const int r = r0 + 64 * j;
+    p.r_lo[j] = op.split == 1 ? r % op.split_n : r;
+    p.r_hi[j] = op.split == 1 ? r / op.split_n : 0;
+  }
+  p.k_lo = op.split == 2 ? k0 % op.split_n : k0;
+  p.k_hi = op.split == 2 ? k0 / op.split_n : 0;
+}
+
+__device__ __forceinline__ void op_advance(const TcOperand& op, OpPos& p) {
+  p.k_lo += kBK;
+  if (op.split == 2 && p.k_lo == op.split_n) {
+    p.k_lo = 0;
+    ++p.k_hi;
+  }
+}
+
+template <int ROWS>
+__device__ __forceinline__ void op_issue(const CUtensorMap* map, const TcOperand& op,
+                                         const OpPos& p, uint8_t* dst, uint64_t* bar) {
   if (!op.mn_major) {
-    const int c0 = op.split == 2 ? k0 % op.split_n : k0;
-    const int c1 = op.split == 1 ? r0 % op.split_n : r0;
-    const int c2 = op.split == 1 ? r0 / op.split_n : (op.split == 2 ? k0 / op.split_n : 0);
-    ptx::tma_load_5d(dst, map, bar, c0, c1, c2, c3, c4);
+    ptx::tma_load_5d(dst, map, bar, p.k_lo, p.r_lo[0], p.r_hi[0] + p.k_hi, p.c3, p.c4);
   } else {
-    // [64 K rows][64 MN] chunks, 8 KB each
-    for (int j = 0; j < rows / 64; ++j) {
-      const int r = r0 + 64 * j;
-      const int c0 = op.split == 1 ? r % op.split_n : r;
-      const int c1 = op.split == 2 ? k0 % op.split_n : k0;
-      const int c2 = op.split == 1 ? r / op.split_n : (op.split == 2 ? k0 / op.split_n : 0);
-      ptx::tma_load_5d(static_cast<char*>(dst) + j * 8192, map, bar, c0, c1, c2, c3, c4);
+#pragma unroll
+    for (int j = 0; j < ROWS / 64; ++j)
+      ptx::tma_load_5d(dst + j * 8192, map, bar, p.r_lo[j], p.k_lo, p.r_hi[j] + p.k_hi, p.c3, p.c4);
+  }
+}
+
+struct Unit {
+  int b, m0, n0, kb0, kb1, ks;
+};
+
+__device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
+  Unit u;
+  // split-major order: the persistent CTAs sweep K window by window together, so each
+  // window's operand footprint stays resident in L2 (no drift-induced thrash).
+  u.ks = t / a.num_tiles;
+  const int tile = t - u.ks * a.num_tiles;
+  const int per_batch = a.m_tiles * a.n_tiles;
+  u.b = tile / per_batch;
+  const int rem = tile - u.b * per_batch;
+  const int mt = rem / a.n_tiles;
+  u.m0 = mt * kBM;
+  u.n0 = (rem - mt * a.n_tiles) * bn;
+  u.kb0 = u.ks * a.kb_per_split;
+  u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
+  return u;
+}
+
+__device__ __forceinline__ void load8(const void* base, int dtype, long long off, float* out) {
+  if (dtype == kF32) {
+    const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
+    const float4 y = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4);
+    out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+    out[4] = y.x; out[5] = y.y; out[6] = y.z; out[7] = y.w;
+  } else {
+    const uint4 q = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      out[2 * i] = f.x;
+      out[2 * i + 1] = f.y;
     }
   }
 }
 
-// Applies the epilogue to one row segment of 32 columns held in v[].
-__device__ __forceinline__ void epilogue_row32(const TcArgs& args, int b, int m, int n0,
+__device__ __forceinline__ void store8(void* base, int dtype, long long off, const float* v) {
+  if (dtype == kF32) {
+    float* p = static_cast<float*>(base) + off;
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+    uint4 pk;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]);
+    __nv_bfloat162 h3 = __floats2bfloat162_rn(v[6], v[7]);
+    pk.x = *reinterpret_cast<uint32_t*>(&h0);
+    pk.y = *reinterpret_cast<uint32_t*>(&h1);
+    pk.z = *reinterpret_cast<uint32_t*>(&h2);
+    pk.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off) = pk;
+  }
+}
+
+// Applies the epilogue to one row segment of 32 columns (v[]) whose first element
+// sits at output offset `off` (column n0).
+__device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off, int n0,
                                                float (&v)[32]) {
   const Epilogue& e = args.epi;
-  const long long row_off = view_offset(e.out, b, m, n0) - n0;
   const int nvalid = min(32, args.N - n0);
+  if (args.vec_ok && nvalid == 32) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    float x = v[j] * e.alpha;
-    if (e.bias != nullptr && j < nvalid) x += __ldg(e.bias + n0 + j);
-    v[j] = x;
-  }
-  if (e.pre_act != nullptr) {
-    if (e.pre_dtype == kF32) {
-      float* p = static_cast<float*>(e.pre_act) + row_off + n0;
-      if (args.vec_ok && nvalid == 32) {
+    for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+    if (e.bias != nullptr) {
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(p + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-      } else {
-        for (int j = 0; j < nvalid; ++j) p[j] = v[j];
-      }
-    } else {
-      __nv_bfloat16* p = static_cast<__nv_bfloat16*>(e.pre_act) + row_off + n0;
-      if (args.vec_ok && nvalid == 32) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 pk;
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-          __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-          __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-          pk.x = *reinterpret_cast<uint32_t*>(&h0);
-          pk.y = *reinterpret_cast<uint32_t*>(&h1);
-          pk.z = *reinterpret_cast<uint32_t*>(&h2);
-          pk.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(p + j) = pk;
-        }
-      } else {
-        for (int j = 0; j < nvalid; ++j) p[j] = __float2bfloat16_rn(v[j]);
+      for (int j = 0; j < 32; j += 4) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + j));
+        v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
       }
     }
-  }
-  if (e.act == kActGelu) {
+    if (e.pre_act != nullptr) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-  } else if (e.act == kActGeluGrad) {
-    for (int j = 0; j < nvalid; ++j) v[j] *= gelu_grad_f(ld_any(e.aux, e.aux_dtype, row_off + n0 + j));
-  }
-  if (e.resid != nullptr) {
-    for (int j = 0; j < nvalid; ++j) v[j] += ld_any(e.resid, e.resid_dtype, row_off + n0 + j);
-  }
-  if (e.accumulate) {
-    for (int j = 0; j < nvalid; ++j) v[j] += ld_any(e.out.base, e.out.dtype, row_off + n0 + j);
-  }
-  if (e.out.dtype == kF32) {
-    float* p = static_cast<float*>(e.out.base) + row_off + n0;
-    if (args.vec_ok && nvalid == 32) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(p + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    } else {
-      for (int j = 0; j < nvalid; ++j) p[j] = v[j];
+      for (int j = 0; j < 32; j += 8) store8(e.pre_act, e.pre_dtype, off + j, v + j);
     }
-  } else {
-    __nv_bfloat16* p = static_cast<__nv_bfloat16*>(e.out.base) + row_off + n0;
-    if (args.vec_ok && nvalid == 32) {
+    if (e.act == kActGelu) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+    } else if (e.act == kActGeluGrad) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
-        uint4 pk;
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&h0);
-        pk.y = *reinterpret_cast<uint32_t*>(&h1);
-        pk.z = *reinterpret_cast<uint32_t*>(&h2);
-        pk.w = *reinterpret_cast<uint32_t*>(&h3);
-        *reinterpret_cast<uint4*>(p + j) = pk;
+        float g[8];
+        load8(e.aux, e.aux_dtype, off + j, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_f(g[i]);
       }
-    } else {
-      for (int j = 0; j < nvalid; ++j) p[j] = __float2bfloat16_rn(v[j]);
     }
+    if (e.resid != nullptr) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float r[8];
+        load8(e.resid, e.resid_dtype, off + j, r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += r[i];
+      }
+    }
+    if (e.accumulate) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float r[8];
+        load8(e.out.base, e.out.dtype, off + j, r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += r[i];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) store8(e.out.base, e.out.dtype, off + j, v + j);
+  } else {
+    for (int j = 0; j < nvalid; ++j) epi_scalar(e, off + j, n0 + j, v[j]);
   }
 }
 
@@ -168,9 +227,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kStageBytes = kABytes + kBBytes;
   constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
   constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+  constexpr int kColsPerWarp = BN / 2;  // two epilogue warps per lane quarter
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the 128B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   const int S = args.stages;
@@ -184,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const int units = args.num_tiles * args.ksplit;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -194,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull_bar[s], 1);
-      ptx::mbar_init(&tempty_bar[s], 4);
+      ptx::mbar_init(&tempty_bar[s], kEpiWarps);
     }
     ptx::fence_barrier_init();
   }
@@ -204,82 +264,116 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int tiles_per_batch = args.m_tiles * args.n_tiles;
-
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      int it = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-        const int b = t / tiles_per_batch;
-        const int rem = t % tiles_per_batch;
-        const int m0 = (rem / args.n_tiles) * kBM;
-        const int n0 = (rem % args.n_tiles) * BN;
-        for (int kb = 0; kb < args.k_blocks; ++kb, ++it) {
-          const int s = it % S;
-          const uint32_t ph = (it / S) & 1;
+      int s = 0;
+      uint32_t ph = 0;
+      OpPos pa, pb;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const Unit u = decode_unit(args, t, BN);
+        op_init(args.a, pa, u.m0, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
+        op_init(args.b, pb, u.n0, B_MN ? BN / 64 : 1, u.kb0 * kBK, u.b);
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          load_operand(&tmA, args.a, smem_a + s * kABytes, &full_bar[s], m0, kBM, kb * kBK, b);
-          load_operand(&tmB, args.b, smem_b + s * kBBytes, &full_bar[s], n0, BN, kb * kBK, b);
+          op_issue<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
+          op_issue<BN>(&tmB, args.b, pb, smem_b + s * kBBytes, &full_bar[s]);
+          op_advance(args.a, pa);
+          op_advance(args.b, pb);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- UMMA issuer
-      int it = 0, tc = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++tc) {
-        const int acc = tc & 1;
-        const uint32_t aph = (tc >> 1) & 1;
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      const uint32_t a0 = ptx::smem_u32(smem_a), b0 = ptx::smem_u32(smem_b);
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const Unit u = decode_unit(args, t, BN);
         ptx::mbar_wait(&tempty_bar[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < args.k_blocks; ++kb, ++it) {
-          const int s = it % S;
-          const uint32_t ph = (it / S) & 1;
+        for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&full_bar[s], ph);
           ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(smem_a + s * kABytes);
-          const uint32_t b_addr = ptx::smem_u32(smem_b + s * kBBytes);
+          const uint32_t a_addr = a0 + s * kABytes;
+          const uint32_t b_addr = b0 + s * kBBytes;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t ad = A_MN ? ptx::smem_desc_sw128(a_addr + k * 2048, 8192, 1024)
                                      : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 8192, 1024)
                                      : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::umma_bf16(tmem_d, ad, bd, kIdesc, (kb > 0 || k > 0) ? 1u : 0u);
+            ptx::umma_bf16(tmem_d, ad, bd, kIdesc, (kb > u.kb0 || k > 0) ? 1u : 0u);
           }
           ptx::umma_commit(&empty_bar[s]);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         ptx::umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
       }
     }
   } else {
-    // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
+    // ---------------- epilogue warps 2..9: lane quarter = warp % 4, column half = (warp-2)/4
     const int quarter = warp & 3;
-    int tc = 0;
-    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++tc) {
-      const int acc = tc & 1;
-      const uint32_t aph = (tc >> 1) & 1;
-      const int b = t / tiles_per_batch;
-      const int rem = t % tiles_per_batch;
-      const int m0 = (rem / args.n_tiles) * kBM;
-      const int n0 = (rem % args.n_tiles) * BN;
+    const int half = (warp - 2) >> 2;
+    int acc = 0;
+    uint32_t aph = 0;
+    const Epilogue& e = args.epi;
+    for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      const Unit u = decode_unit(args, t, BN);
+      const int m = u.m0 + quarter * 32 + lane;
+      // row offset once per unit (the only divisions on the epilogue path)
+      long long row_off = 0;
+      if (args.ksplit > 1) row_off = (static_cast<long long>(u.ks) * args.M + m) * args.N;
+      else if (m < args.M) row_off = view_offset(e.out, u.b, m, 0);
       ptx::mbar_wait(&tfull_bar[acc], aph);
       ptx::tc_fence_after();
-      const int m = m0 + quarter * 32 + lane;
-      const uint32_t row_taddr = tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16);
+      const uint32_t row_taddr =
+          tmem_base + acc * BN + (static_cast<uint32_t>(quarter * 32) << 16) + half * kColsPerWarp;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < kColsPerWarp / 32; ++c) {
         float v[32];
         ptx::tmem_ld32(row_taddr + c * 32, v);
-        const int nc = n0 + c * 32;
-        if (m < args.M && nc < args.N) epilogue_row32(args, b, m, nc, v);
+        const int nc = u.n0 + half * kColsPerWarp + c * 32;
+        if (m < args.M && nc < args.N) {
+          if (args.ksplit > 1) {
+            float* p = args.ws + row_off + nc;
+            const int nvalid = min(32, args.N - nc);
+            if (nvalid == 32 && args.vec_ok) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) store8(p, kF32, j, v + j);
+            } else {
+              for (int j = 0; j < nvalid; ++j) p[j] = v[j];
+            }
+          } else {
+            long long off = row_off + nc;
+            if (e.out.csplit) off = row_off + (nc % e.out.csplit) + (nc / e.out.csplit) * e.out.s_hi;
+            epilogue_row32(args, off, nc, v);
+          }
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aph ^= 1;
+      }
     }
   }
 
@@ -287,6 +381,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// Split-K reduction: out = epilogue(sum_k ws[k][m][n]) in ascending split order.
+__global__ void splitk_reduce_kernel(const float* ws, int ksplit, int M, int N, Epilogue e) {
+  const long long total = static_cast<long long>(M) * N;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < ksplit; ++k) acc += ws[k * total + t];
+    const long long m = t / N, n = t - (t / N) * N;
+    epi_scalar(e, view_offset(e.out, 0, m, n), n, acc);
   }
 }
 
@@ -386,7 +492,7 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcArgs& args, int n
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
     attr_set = true;
   }
-  const int grid = std::min(args.num_tiles, num_sms);
+  const int grid = std::min(args.num_tiles * args.ksplit, num_sms);
   kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
 }
 
@@ -416,19 +522,45 @@ bool operand_ok(const View& v, long long rows, long long cols, int tile_rows) {
     if (v.rsplit % (mn ? 64 : tile_rows)) return false;
   }
   if (v.csplit && v.csplit % 64) return false;
-  // MN-major tiles are loaded in 64-wide chunks: the r extent must cover whole chunks of
-  // the tile or be padded by TMA out-of-bounds fill, which is fine.
   return true;
+}
+
+// Picks the number of K splits for a batch-1 problem with few output tiles: only
+// when fewer than half the SMs would get a tile, maximising wave efficiency
+// (units / (waves * SMs)) with >= 16 K-blocks per split (measured on B200: splitting
+// a 128-tile GEMM loses to the extra partial-sum traffic; a 32-tile one gains 2x).
+int pick_ksplit(long long M, long long N, int tiles, int k_blocks, int batch, int num_sms) {
+  (void)M;
+  (void)N;
+  if (const char* env = std::getenv("C3D_KSPLIT")) {  // experiments only
+    const int ks = std::atoi(env);
+    if (ks >= 1 && batch == 1) return std::min(ks, std::max(1, k_blocks / 4));
+  }
+  if (batch != 1 || 2 * tiles > num_sms) return 1;
+  int best = 1;
+  double best_eff = static_cast<double>(tiles) / num_sms;
+  for (int ks = 2; ks <= 8; ++ks) {
+    if (k_blocks / ks < 16) break;
+    const int units = tiles * ks;
+    const int waves = (units + num_sms - 1) / num_sms;
+    const double eff = static_cast<double>(units) / (waves * num_sms) - 0.01 * ks;
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = ks;
+    }
+  }
+  return best;
 }
 
 }  // namespace
 
 int tc_pick_bn(long long M, long long N, int batch, int num_sms) {
+  (void)M;
+  (void)batch;
+  (void)num_sms;
   if (N <= 64) return 64;
   if (N <= 128) return 128;
-  const long long mt = (M + kBM - 1) / kBM;
-  const long long tiles256 = mt * ((N + 255) / 256) * batch;
-  if (N % 256 == 0 && tiles256 >= num_sms) return 256;
+  if (N % 256 == 0) return 256;
   return 128;
 }
 
@@ -452,25 +584,43 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.n_tiles = static_cast<int>((p.N + bn - 1) / bn);
   args.k_blocks = static_cast<int>((p.K + kBK - 1) / kBK);
   args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
+  args.ksplit = pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms);
+  args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
+  args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
   args.epi = p.epi;
-  // vector stores need 16-B aligned rows
+  // vector loads/stores need 16-B aligned rows and 32-column chunks
   const int esz = p.epi.out.dtype == kF32 ? 4 : 2;
-  bool vec = reinterpret_cast<uintptr_t>(p.epi.out.base) % 16 == 0 &&
-             (p.epi.out.sr * esz) % 16 == 0 && (p.epi.out.s_hi * esz) % 16 == 0 &&
-             (p.epi.out.sb_lo * esz) % 16 == 0 && (p.epi.out.sb_hi * esz) % 16 == 0;
-  if (p.epi.pre_act) {
-    const int pz = p.epi.pre_dtype == kF32 ? 4 : 2;
-    vec = vec && reinterpret_cast<uintptr_t>(p.epi.pre_act) % 16 == 0 &&
-          (p.epi.out.sr * pz) % 16 == 0;
-  }
+  auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  bool vec = al(p.epi.out.base) && (p.epi.out.sr * esz) % 16 == 0 &&
+             (p.epi.out.s_hi * esz) % 16 == 0 && (p.epi.out.sb_lo * esz) % 16 == 0 &&
+             (p.epi.out.sb_hi * esz) % 16 == 0 && (p.epi.out.csplit % 32) == 0;
+  const int sizes[3] = {p.epi.pre_dtype == kF32 ? 4 : 2, p.epi.aux_dtype == kF32 ? 4 : 2,
+                        p.epi.resid_dtype == kF32 ? 4 : 2};
+  const void* ptrs[3] = {p.epi.pre_act, p.epi.aux, p.epi.resid};
+  for (int i = 0; i < 3; ++i)
+    if (ptrs[i]) vec = vec && al(ptrs[i]) && (p.epi.out.sr * sizes[i]) % 16 == 0;
+  if (p.epi.bias) vec = vec && al(p.epi.bias);
+  if (args.ksplit > 1) vec = vec && (p.N % 4 == 0);
   args.vec_ok = vec ? 1 : 0;
   CUtensorMap ma = make_operand_map(p.a, p.M, p.K, p.batch, kBM, &args.a);
   CUtensorMap mb = make_operand_map(p.b, p.N, p.K, p.batch, bn, &args.b);
+  float* ws = nullptr;
+  if (args.ksplit > 1) {
+    C3D_CUDA(cudaMallocAsync(&ws, sizeof(float) * args.ksplit * p.M * p.N, stream));
+    args.ws = ws;
+  }
   switch (bn) {
     case 64: launch_bn<64>(ma, mb, args, num_sms, stream); break;
     case 128: launch_bn<128>(ma, mb, args, num_sms, stream); break;
     case 256: launch_bn<256>(ma, mb, args, num_sms, stream); break;
     default: throw std::runtime_error("tc_gemm: unsupported BN");
+  }
+  if (args.ksplit > 1) {
+    check_launch("tc_gemm(split-k)");
+    const long long total = p.M * p.N;
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, args.ksplit, args.M, args.N, p.epi);
+    C3D_CUDA(cudaFreeAsync(ws, stream));
   }
 }
 
