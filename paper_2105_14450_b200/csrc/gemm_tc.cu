@@ -58,9 +58,58 @@ struct TcArgs {
   int stages;
   int vec_ok;
   float* ws;  // split-K partials [ksplit][M][N] fp32
+  // TMA-store epilogue: output tile chunks [32 rows][128 B] staged in swizzled smem
+  int tma_store;             // 1: stores go through tmC / tmP
+  int cw;                    // columns per store chunk (32 fp32, 64 bf16)
+  int st_rsplit, st_csplit;  // split of the stored view (rows / cols)
+  int st_blo;                // batch-lo extent of the stored view
   TcOperand a, b;
   Epilogue epi;
 };
+
+// Writes one 32-value row segment (CW = 32 fp32 or 64 bf16 values = 128 B) into row
+// `lane` of a [32][128 B] tile laid out with the TMA 128B swizzle (16-B chunk j of row
+// r lives at chunk j ^ (r & 7)); conflict-free for a warp writing one row per lane.
+template <int CW>
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
+  uint8_t* row = buf + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint8_t* dst = row + ((j ^ (lane & 7)) << 4);
+    if (CW == 32) {
+      *reinterpret_cast<float4*>(dst) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    } else {
+      uint4 pk;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+      pk.x = *reinterpret_cast<uint32_t*>(&h0);
+      pk.y = *reinterpret_cast<uint32_t*>(&h1);
+      pk.z = *reinterpret_cast<uint32_t*>(&h2);
+      pk.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(dst) = pk;
+    }
+  }
+}
+
+// Makes the staged tile visible to the async proxy and issues its TMA store.
+__device__ __forceinline__ void store_staged(const CUtensorMap* map, const uint8_t* buf, int lane,
+                                             int c0, int c1, int c2, int c3, int c4) {
+  ptx::fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    ptx::tma_store_5d(map, buf, c0, c1, c2, c3, c4);
+    ptx::bulk_commit();
+  }
+}
+
+// Waits until this warp's staging buffer may be rewritten.
+__device__ __forceinline__ void staging_acquire(int lane) {
+  if (lane == 0) ptx::bulk_wait_read();
+  __syncwarp();
+}
 
 // TMA coordinates of one operand for the current tile, advanced per K-block.
 struct OpPos {
@@ -214,14 +263,114 @@ __device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off
 #pragma unroll
     for (int j = 0; j < 32; j += 8) store8(e.out.base, e.out.dtype, off + j, v + j);
   } else {
-    for (int j = 0; j < nvalid; ++j) epi_scalar(e, off + j, n0 + j, v[j]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) epi_scalar(e, off + j, n0 + j, v[j]);
+  }
+}
+
+// Epilogue math on CW values of one output row starting at column n0; `off` is the
+// element offset of (m, n0) for aux/resid/accumulate loads (valid when row_ok).
+// A requested pre-activation store goes through the staging buffer and tmP.
+template <int CW>
+__device__ __forceinline__ void epi_math_tma(const TcArgs& args, long long off, int n0, float* v,
+                                             bool row_ok, const CUtensorMap* tmP, uint8_t* buf,
+                                             int lane, int c0, int c1, int c2, int c3, int c4) {
+  const Epilogue& e = args.epi;
+  const bool full = n0 + CW <= args.N;
+  const int nvalid = min(CW, args.N - n0);
+#pragma unroll
+  for (int j = 0; j < CW; ++j) v[j] *= e.alpha;
+  if (e.bias != nullptr) {
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < CW; j += 4) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + j));
+        v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+        if (j < nvalid) v[j] += e.bias[n0 + j];
+    }
+  }
+  if (e.pre_act != nullptr) {
+    staging_acquire(lane);
+    stage_row<CW>(buf, lane, v);
+    store_staged(tmP, buf, lane, c0, c1, c2, c3, c4);
+  }
+  const bool vec = full && row_ok && args.vec_ok;
+  if (e.act == kActGelu) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) v[j] = gelu_f(v[j]);
+  } else if (e.act == kActGeluGrad && row_ok) {
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < CW; j += 8) {
+        float g[8];
+        load8(e.aux, e.aux_dtype, off + j, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_f(g[i]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+        if (j < nvalid) v[j] *= gelu_grad_f(ld_any(e.aux, e.aux_dtype, off + j));
+    }
+  }
+  if (e.resid != nullptr && row_ok) {
+    if (vec) {
+#pragma unroll
+      for (int j = 0; j < CW; j += 8) {
+        float r[8];
+        load8(e.resid, e.resid_dtype, off + j, r);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += r[i];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+        if (j < nvalid) v[j] += ld_any(e.resid, e.resid_dtype, off + j);
+    }
+  }
+  if (e.accumulate && row_ok) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+      if (j < nvalid) v[j] += ld_any(e.out.base, e.out.dtype, off + j);
+  }
+}
+
+template <int CW, int COLS>
+__device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorMap* tmC,
+                                             const CUtensorMap* tmP, uint8_t* buf, int lane,
+                                             uint32_t row_taddr, int ncol0, long long row_off,
+                                             bool row_ok, int c1, int c2r, int c3, int c4) {
+  const Epilogue& e = args.epi;
+#pragma unroll 1
+  for (int cc = 0; cc < COLS / CW; ++cc) {
+    float v[CW];
+    ptx::tmem_ld32(row_taddr + cc * CW, *reinterpret_cast<float(*)[32]>(v));
+    if (CW == 64) ptx::tmem_ld32(row_taddr + cc * CW + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+    const int n = ncol0 + cc * CW;
+    if (n >= args.N) continue;  // warp-uniform
+    const int c0 = args.st_csplit ? n % args.st_csplit : n;
+    const int c2 = c2r + (args.st_csplit ? n / args.st_csplit : 0);
+    if (args.ksplit == 1) {
+      const long long off = row_off + (e.out.csplit ? (n % e.out.csplit) + (n / e.out.csplit) * e.out.s_hi : n);
+      epi_math_tma<CW>(args, off, n, v, row_ok, tmP, buf, lane, c0, c1, c2, c3, c4);
+    }
+    staging_acquire(lane);
+    stage_row<CW>(buf, lane, v);
+    store_staged(tmC, buf, lane, c0, c1, c2, c3, c4);
   }
 }
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC,
+                   const __grid_constant__ CUtensorMap tmP, const TcArgs args) {
   constexpr int kABytes = kBM * kBK * 2;  // 16 KB
   constexpr int kBBytes = BN * kBK * 2;
   constexpr int kStageBytes = kABytes + kBBytes;
@@ -235,7 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = args.stages;
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStageBytes);
+  uint8_t* smem_stage = smem + S * kStageBytes;  // 8 epilogue warps x 4 KB, 1024-aligned
+  uint64_t* full_bar =
+      reinterpret_cast<uint64_t*>(smem + S * kStageBytes + (args.tma_store ? kEpiWarps * 4096 : 0));
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -334,6 +485,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     const Epilogue& e = args.epi;
+    if (args.tma_store) {
+      uint8_t* buf = smem_stage + (warp - 2) * 4096;
+      const bool need_off =
+          args.ksplit == 1 && (e.aux != nullptr || e.resid != nullptr || e.accumulate);
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const Unit u = decode_unit(args, t, BN);
+        const int mrow0 = u.m0 + quarter * 32;
+        const int m = mrow0 + lane;
+        const bool row_ok = m < args.M;
+        const long long row_off = (need_off && row_ok) ? view_offset(e.out, u.b, m, 0) : 0;
+        const int bidx = args.ksplit > 1 ? u.ks : u.b;
+        const int c3 = bidx % args.st_blo, c4 = bidx / args.st_blo;
+        const int c1 = args.st_rsplit ? mrow0 % args.st_rsplit : mrow0;
+        const int c2r = args.st_rsplit ? mrow0 / args.st_rsplit : 0;
+        ptx::mbar_wait(&tfull_bar[acc], aph);
+        ptx::tc_fence_after();
+        const uint32_t row_taddr = tmem_base + acc * BN +
+                                   (static_cast<uint32_t>(quarter * 32) << 16) + half * kColsPerWarp;
+        const int ncol0 = u.n0 + half * kColsPerWarp;
+        if (args.cw == 32)
+          epi_tile_tma<32, kColsPerWarp>(args, &tmC, &tmP, buf, lane, row_taddr, ncol0, row_off,
+                                         row_ok, c1, c2r, c3, c4);
+        else
+          epi_tile_tma<(kColsPerWarp >= 64 ? 64 : 32), kColsPerWarp>(
+              args, &tmC, &tmP, buf, lane, row_taddr, ncol0, row_off, row_ok, c1, c2r, c3, c4);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1;
+        }
+      }
+      if (lane == 0) ptx::bulk_wait_all();
+    } else
     for (int t = blockIdx.x; t < units; t += gridDim.x) {
       const Unit u = decode_unit(args, t, BN);
       const int m = u.m0 + quarter * 32 + lane;
@@ -358,7 +544,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 32; j += 8) store8(p, kF32, j, v + j);
             } else {
-              for (int j = 0; j < nvalid; ++j) p[j] = v[j];
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < nvalid) p[j] = v[j];
             }
           } else {
             long long off = row_off + nc;
@@ -478,14 +666,51 @@ CUtensorMap make_operand_map(const View& v, long long rows, long long cols, int 
   return map;
 }
 
+// Output store map: 5-D view of the stored tensor (cols, rows, split-hi, batch-lo,
+// batch-hi), box [32 rows][128 B], 128B swizzle. Returns false when the view is not
+// TMA-addressable (the kernel then stores directly from registers).
+bool make_store_map(const View& v, long long rows, long long cols, int batch, int cw,
+                    CUtensorMap* map) {
+  const long long es = v.dtype == kF32 ? 4 : 2;
+  if (v.sc != 1 || reinterpret_cast<uintptr_t>(v.base) % 16) return false;
+  if (v.rsplit && v.csplit) return false;
+  if (v.rsplit && v.rsplit % 32) return false;
+  if (v.csplit && v.csplit % cw) return false;
+  for (long long s : {v.sr, v.s_hi, v.sb_lo, v.sb_hi})
+    if ((s * es) % 16) return false;
+  const long long rlo = v.rsplit ? v.rsplit : rows;
+  const long long clo = v.csplit ? v.csplit : cols;
+  const long long nhi = v.rsplit ? (rows + v.rsplit - 1) / v.rsplit
+                                 : (v.csplit ? (cols + v.csplit - 1) / v.csplit : 1);
+  const long long bhi = (batch + v.b_lo_n - 1) / v.b_lo_n;
+  cuuint64_t dims[5] = {static_cast<cuuint64_t>(clo), static_cast<cuuint64_t>(rlo),
+                        static_cast<cuuint64_t>(nhi), static_cast<cuuint64_t>(v.b_lo_n),
+                        static_cast<cuuint64_t>(bhi)};
+  const long long fb = std::max<long long>(16, v.sr * es * rlo);
+  cuuint64_t strides[4] = {static_cast<cuuint64_t>(v.sr * es),
+                           static_cast<cuuint64_t>(v.s_hi ? v.s_hi * es : fb),
+                           static_cast<cuuint64_t>(v.sb_lo ? v.sb_lo * es : fb),
+                           static_cast<cuuint64_t>(v.sb_hi ? v.sb_hi * es : fb)};
+  if (rows == 1 || rlo == 1) strides[0] = std::max<cuuint64_t>(strides[0], 16);
+  cuuint32_t box[5] = {static_cast<cuuint32_t>(cw), 32, 1, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  std::memset(map, 0, sizeof(*map));
+  const CUresult r = encode_fn()(
+      map, v.dtype == kF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+      v.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int BN, bool A_MN, bool B_MN>
-void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcArgs& args, int num_sms,
-               cudaStream_t stream) {
+void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+               const CUtensorMap& mp, TcArgs& args, int num_sms, cudaStream_t stream) {
   constexpr int kStageBytes = (kBM + BN) * kBK * 2;
-  int stages = (kSmemBudget - 1024 - 256) / kStageBytes;
+  const int staging = args.tma_store ? kEpiWarps * 4096 : 0;
+  int stages = (kSmemBudget - 1024 - 256 - staging) / kStageBytes;
   stages = std::min(stages, 8);
   args.stages = stages;
-  const int smem = 1024 + stages * kStageBytes + (2 * stages + 4) * 8 + 16;
+  const int smem = 1024 + stages * kStageBytes + staging + (2 * stages + 4) * 8 + 16;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -493,17 +718,17 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, TcArgs& args, int n
     attr_set = true;
   }
   const int grid = std::min(args.num_tiles * args.ksplit, num_sms);
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mp, args);
 }
 
 template <int BN>
-void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, TcArgs& args, int num_sms,
-               cudaStream_t stream) {
+void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+               const CUtensorMap& mp, TcArgs& args, int num_sms, cudaStream_t stream) {
   const bool am = args.a.mn_major, bm = args.b.mn_major;
-  if (!am && !bm) launch_tc<BN, false, false>(ma, mb, args, num_sms, stream);
-  else if (!am && bm) launch_tc<BN, false, true>(ma, mb, args, num_sms, stream);
-  else if (am && !bm) launch_tc<BN, true, false>(ma, mb, args, num_sms, stream);
-  else launch_tc<BN, true, true>(ma, mb, args, num_sms, stream);
+  if (!am && !bm) launch_tc<BN, false, false>(ma, mb, mc, mp, args, num_sms, stream);
+  else if (!am && bm) launch_tc<BN, false, true>(ma, mb, mc, mp, args, num_sms, stream);
+  else if (am && !bm) launch_tc<BN, true, false>(ma, mb, mc, mp, args, num_sms, stream);
+  else launch_tc<BN, true, true>(ma, mb, mc, mp, args, num_sms, stream);
 }
 
 bool operand_ok(const View& v, long long rows, long long cols, int tile_rows) {
@@ -609,10 +834,39 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     C3D_CUDA(cudaMallocAsync(&ws, sizeof(float) * args.ksplit * p.M * p.N, stream));
     args.ws = ws;
   }
+  // TMA-store epilogue when the stored view (output, or the split-K workspace) and the
+  // optional pre-activation output are TMA-addressable.
+  CUtensorMap mc, mp;
+  std::memset(&mc, 0, sizeof(mc));
+  std::memset(&mp, 0, sizeof(mp));
+  View sv = p.epi.out;
+  int sbatch = p.batch;
+  if (args.ksplit > 1) {
+    sv = View();
+    sv.base = ws;
+    sv.dtype = kF32;
+    sv.sr = p.N;
+    sv.sb_lo = p.M * p.N;
+    sv.b_lo_n = args.ksplit;
+    sbatch = args.ksplit;
+  }
+  args.cw = sv.dtype == kF32 ? 32 : 64;
+  bool tma = !std::getenv("C3D_NO_TMA_STORE") && args.cw <= bn / 2 &&
+             make_store_map(sv, p.M, p.N, sbatch, args.cw, &mc);
+  if (tma && args.ksplit == 1 && p.epi.pre_act) {
+    View pv = p.epi.out;
+    pv.base = p.epi.pre_act;
+    pv.dtype = p.epi.pre_dtype;
+    tma = pv.dtype == sv.dtype && make_store_map(pv, p.M, p.N, p.batch, args.cw, &mp);
+  }
+  args.tma_store = tma ? 1 : 0;
+  args.st_rsplit = static_cast<int>(sv.rsplit);
+  args.st_csplit = static_cast<int>(sv.csplit);
+  args.st_blo = sv.b_lo_n;
   switch (bn) {
-    case 64: launch_bn<64>(ma, mb, args, num_sms, stream); break;
-    case 128: launch_bn<128>(ma, mb, args, num_sms, stream); break;
-    case 256: launch_bn<256>(ma, mb, args, num_sms, stream); break;
+    case 64: launch_bn<64>(ma, mb, mc, mp, args, num_sms, stream); break;
+    case 128: launch_bn<128>(ma, mb, mc, mp, args, num_sms, stream); break;
+    case 256: launch_bn<256>(ma, mb, mc, mp, args, num_sms, stream); break;
     default: throw std::runtime_error("tc_gemm: unsupported BN");
   }
   if (args.ksplit > 1) {
