@@ -377,8 +377,14 @@ def our_arm(args, wl):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    cube.close()
-    return 0
+    # Captured graphs still reference the NCCL communicators, and tearing those down
+    # under live graphs can block; every rank is past its last collective after this
+    # barrier, so leave process teardown to the OS.
+    torch.cuda.synchronize()
+    dist.barrier()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 def main():
