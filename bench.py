@@ -214,14 +214,21 @@ def our_arm(args, wl):
         outs["y"], outs["dx"] = y, dx
         return y, dx
 
-    # eager warm-up: at least W steps and ~1 s, so SM clocks leave their idle state
-    warm = 0
+    # eager warm-up: at least W steps and ~1 s, so SM clocks leave their idle state.
+    # The step count is agreed across ranks (every step issues collectives).
+    warm = max(args.warmup, 3)
     t0 = time.time()
-    while warm < max(args.warmup, 3) or time.time() - t0 < 1.0:
+    for _ in range(warm):
         step(x, dy)
-        warm += 1
-        if warm % 4 == 0:
+    torch.cuda.synchronize()
+    spent = dist.max_over_ranks(time.time() - t0)
+    extra = 0 if spent >= 1.0 else int((1.0 - spent) / max(spent / warm, 1e-4)) + 1
+    extra = int(dist.max_over_ranks(float(min(extra, 2000))))
+    for i in range(extra):
+        step(x, dy)
+        if i % 8 == 7:
             torch.cuda.synchronize()
+    warm += extra
     torch.cuda.synchronize()
     # eager (per-op launch) timing, for reference
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

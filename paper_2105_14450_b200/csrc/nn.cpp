@@ -75,7 +75,8 @@ void validate_config(const Cube& cube, const Config& cfg) {
 // ------------------------------------------------------------------ Linear
 
 void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group, Act& y,
-                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s) {
+                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s,
+                const LinearPre* pre) {
   // linear3d_fwd (cube3d/nn.hpp:81-97)
   if (x.group != group)
     fail(C3D_ERR_GROUP_MISMATCH, "activation group " + std::to_string(x.group) +
@@ -93,13 +94,19 @@ void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group
   if (p.b.len != p.w.gcols)
     fail(C3D_ERR_SHAPE_MISMATCH, "vector length " + std::to_string(p.b.len) +
                                      " does not match matrix cols " + std::to_string(p.w.gcols));
-  DevBuf bias = expand_diagonal(cube, xf.dirs.swapped(), p.b, s);
+  DevBuf bias;
+  LinearEpi e = extra;
+  if (pre && pre->bias) {
+    e.bias = pre->bias;
+  } else {
+    bias = expand_diagonal(cube, xf.dirs.swapped(), p.b, s);
+    e.bias = bias.as<float>();
+  }
   Mat c;
   c.data = y.data;
   c.dtype = y.dtype;
-  LinearEpi e = extra;
-  e.bias = bias.as<float>();
-  ab_forward(cube, mode, xf, p.w, c, e, s);
+  ab_forward(cube, mode, xf, p.w, c, e, s, pre ? &pre->wg : nullptr,
+             saved ? &saved->a_full : nullptr);
   group = 1 - group;
   y = make_act(cube, y.data, y.dtype, x.batch, x.seq, p.w.gcols, group);
   if (saved) {
@@ -110,11 +117,14 @@ void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group
                                cudaMemcpyDeviceToDevice, s));
       saved->x.data = cp.get();
     }
+    // keep the gathered input only when it is a buffer of our own (p_in > 1)
+    if (saved->a_full.buf.get() == nullptr) saved->a_full.ptr = nullptr;
   }
 }
 
 void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, const LinearP& p,
-                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s) {
+                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s,
+                const Operand* wg, const LinearSinks* sinks) {
   // linear3d_bwd (cube3d/nn.hpp:99-112): add_vec_bwd then matmul_ab_bwd.
   if (dy.group != 1 - p.input_group)
     fail(C3D_ERR_GROUP_MISMATCH, "upstream gradient group does not match the layer output group");
@@ -123,7 +133,9 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
     fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB backward must carry the swapped triple");
   // The reduction is collective: every rank joins it whether or not it holds a
   // diagonal slice (non-holders pass a vector with no local data).
-  if (db) {
+  if (sinks && sinks->bias_colsum) {
+    k_colsum(dyf.data, dyf.dtype, nullptr, kF32, dyf.rows, dyf.cols, sinks->bias_colsum, s);
+  } else if (db) {
     DevBuf cs(static_cast<size_t>(dyf.cols) * sizeof(float), s);
     k_colsum(dyf.data, dyf.dtype, nullptr, kF32, dyf.rows, dyf.cols, cs.as<float>(), s);
     Vec out = *db;
@@ -136,28 +148,35 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
     da.dtype = dx->dtype;
     dap = &da;
   }
-  ab_backward(cube, mode, dyf, saved.x, p.w, dap, dw, dx_gelu_aux, s);
+  ab_backward(cube, mode, dyf, saved.x, p.w, dap, dw, dx_gelu_aux, s, wg, saved.a_full.ptr,
+              sinks ? &sinks->dw : nullptr);
   if (dap) *dx = make_act(cube, dx->data, dx->dtype, dy.batch, dy.seq, saved.x.gcols, p.input_group);
 }
 
 // --------------------------------------------------------------- LayerNorm
 
 void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, double eps,
-                   Act& y, LNSaved* saved, cudaStream_t s) {
+                   Act& y, LNSaved* saved, cudaStream_t s, const float* gpre,
+                   const float* bpre) {
   // layernorm3d_fwd (cube3d/nn.hpp:140-185)
   if (gamma.len != x.hidden || beta.len != x.hidden)
     fail(C3D_ERR_SHAPE_MISMATCH, "layer norm parameter length does not match hidden size");
   const Dirs d = triple_for_group(x.group);
   const int Pout = cube.extent(d.out);
   const float inv_h = 1.f / static_cast<float>(x.hidden);
-  DevBuf gblock = expand_diagonal(cube, d, gamma, s);
-  DevBuf bblock = expand_diagonal(cube, d, beta, s);
+  DevBuf gown, bown;
+  if (!gpre || !bpre) {
+    gown = expand_diagonal(cube, d, gamma, s);
+    bown = expand_diagonal(cube, d, beta, s);
+  }
+  const float* gb = gpre ? gpre : gown.as<float>();
+  const float* bb = bpre ? bpre : bown.as<float>();
   y = make_act(cube, y.data, y.dtype, x.batch, x.seq, x.hidden, x.group);
   DevBuf xhat(x.elems() * dtype_size(x.dtype), s);
   DevBuf inv_std(static_cast<size_t>(x.rows) * sizeof(float), s);
   if (Pout == 1) {
-    k_ln_fwd_fused(x.data, x.dtype, x.rows, x.cols, static_cast<float>(eps), gblock.as<float>(),
-                   bblock.as<float>(), y.data, y.dtype, xhat.get(), x.dtype, inv_std.as<float>(), s);
+    k_ln_fwd_fused(x.data, x.dtype, x.rows, x.cols, static_cast<float>(eps), gb, bb, y.data,
+                   y.dtype, xhat.get(), x.dtype, inv_std.as<float>(), s);
   } else {
     DevBuf sums(static_cast<size_t>(x.rows) * sizeof(float), s);
     DevBuf sq(static_cast<size_t>(x.rows) * sizeof(float), s);
@@ -166,8 +185,8 @@ void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, 
     k_row_sum(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), inv_h, sq.as<float>(), s);
     cube.all_reduce(d.out, sq.get(), x.rows, kF32, false, s);
     k_ln_apply(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), sq.as<float>(), inv_h,
-               static_cast<float>(eps), gblock.as<float>(), bblock.as<float>(), y.data, y.dtype,
-               xhat.get(), x.dtype, inv_std.as<float>(), s);
+               static_cast<float>(eps), gb, bb, y.data, y.dtype, xhat.get(), x.dtype,
+               inv_std.as<float>(), s);
   }
   if (saved) {
     saved->dtype = x.dtype;
@@ -175,18 +194,21 @@ void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, 
     saved->hidden = x.hidden;
     saved->xhat = saved->keep(std::move(xhat)).get();
     saved->inv_std = saved->keep(std::move(inv_std)).as<float>();
-    saved->gamma_block = saved->keep(std::move(gblock)).as<float>();
+    saved->gamma_block = gpre ? const_cast<float*>(gpre) : saved->keep(std::move(gown)).as<float>();
   }
 }
 
 void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const Vec* dgamma,
-                   const Vec* dbeta, const void* resid, cudaStream_t s) {
+                   const Vec* dbeta, const void* resid, cudaStream_t s, float* sink) {
   // layernorm3d_bwd (cube3d/nn.hpp:187-222)
   if (dy.group != sv.group || dy.hidden != sv.hidden)
     fail(C3D_ERR_SHAPE_MISMATCH, "layer norm gradient does not match the saved forward");
   const Dirs d = triple_for_group(dy.group);
   const float inv_h = 1.f / static_cast<float>(dy.hidden);
-  if (dgamma && dbeta) {  // collective on every rank (see linear_bwd)
+  if (sink) {
+    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, sink, s);
+    k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, sink + dy.cols, s);
+  } else if (dgamma && dbeta) {  // collective on every rank (see linear_bwd)
     DevBuf cs(static_cast<size_t>(2 * dy.cols) * sizeof(float), s);
     k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, cs.as<float>(), s);
     k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, cs.as<float>() + dy.cols, s);
@@ -284,7 +306,8 @@ View packed_out(void* base, int dtype, const AttnDims& a, bool split) {
 
 void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& qkv_p,
                    const LinearP& out_p, int& group, Act& y, AttnSaved* sv, bool own_input,
-                   const void* resid, cudaStream_t s) {
+                   const void* resid, cudaStream_t s, const LinearPre* qkv_pre,
+                   const LinearPre* out_pre) {
   // attention_fwd (cube3d/attention.hpp:78-136)
   validate_config(cube, cfg);
   if (x.hidden != cfg.hidden) fail(C3D_ERR_SHAPE_MISMATCH, "attention input hidden size mismatch");
@@ -297,7 +320,7 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
   Act qkv;
   qkv.data = qkv_buf.get();
   qkv.dtype = dt;
-  linear_fwd(cube, mode, x, qkv_p, group, qkv, &S.qkv_lin, own_input, LinearEpi{}, s);
+  linear_fwd(cube, mode, x, qkv_p, group, qkv, &S.qkv_lin, own_input, LinearEpi{}, s, qkv_pre);
   const AttnDims a = attn_dims(cube, cfg, qkv.group);
   if (qkv.cols != a.ld_qkv) fail(C3D_ERR_SHAPE_MISMATCH, "qkv projection width mismatch");
   S.qkv = qkv;
@@ -359,12 +382,13 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
   }
   LinearEpi oe;
   oe.resid = resid;
-  linear_fwd(cube, mode, ctx, out_p, group, y, &S.out_lin, false, oe, s);
+  linear_fwd(cube, mode, ctx, out_p, group, y, &S.out_lin, false, oe, s, out_pre);
 }
 
 void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const AttnSaved& S,
                    const LinearP& qkv_p, const LinearP& out_p, Act& dx, LayerG& g,
-                   cudaStream_t s) {
+                   cudaStream_t s, const Operand* qkv_wg, const Operand* out_wg,
+                   const LinearSinks* qkv_sinks, const LinearSinks* out_sinks) {
   // attention_bwd (cube3d/attention.hpp:138-189)
   const int dt = dy.dtype;
   const ActGeom cg = act_geom(cube.grid(), dy.batch, dy.seq, cfg.hidden, 1 - dy.group);
@@ -372,7 +396,8 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
   Act dctx;
   dctx.data = dctx_buf.get();
   dctx.dtype = dt;
-  linear_bwd(cube, mode, dy, S.out_lin, out_p, &dctx, &g.w_out, &g.b_out, nullptr, s);
+  linear_bwd(cube, mode, dy, S.out_lin, out_p, &dctx, &g.w_out, &g.b_out, nullptr, s, out_wg,
+             out_sinks);
   const AttnDims a = attn_dims(cube, cfg, dctx.group);
   const int64_t rows = a.bl * a.sl;
   const int nslices = static_cast<int>(a.bl * a.H);
@@ -432,14 +457,16 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
     gemm_views(cube, mode, a.sl, a.dh, a.S, nslices, scores_view(dp.get(), dt, a, true), qv, e, s);
   }
   Act dqkv = make_act(cube, dqkv_buf.get(), dt, dy.batch, dy.seq, 3 * cfg.hidden, dctx.group);
-  linear_bwd(cube, mode, dqkv, S.qkv_lin, qkv_p, &dx, &g.w_qkv, &g.b_qkv, nullptr, s);
+  linear_bwd(cube, mode, dqkv, S.qkv_lin, qkv_p, &dx, &g.w_qkv, &g.b_qkv, nullptr, s, qkv_wg,
+             qkv_sinks);
 }
 
 // --------------------------------------------------------------------- MLP
 
 void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& fc1,
              const LinearP& fc2, int& group, Act& y, MlpSaved* sv, bool own_input,
-             const void* resid, cudaStream_t s) {
+             const void* resid, cudaStream_t s, const LinearPre* fc1_pre,
+             const LinearPre* fc2_pre) {
   // mlp_fwd (cube3d/transformer.hpp:44-53); GELU fused into the FC1 epilogue.
   MlpSaved local;
   MlpSaved& S = sv ? *sv : local;
@@ -453,14 +480,16 @@ void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const Linear
   LinearEpi e1;
   e1.act = kActGelu;
   e1.pre_act = S.pre_act;
-  linear_fwd(cube, mode, x, fc1, group, h1, &S.fc1_lin, own_input, e1, s);
+  linear_fwd(cube, mode, x, fc1, group, h1, &S.fc1_lin, own_input, e1, s, fc1_pre);
   LinearEpi e2;
   e2.resid = resid;
-  linear_fwd(cube, mode, h1, fc2, group, y, &S.fc2_lin, false, e2, s);
+  linear_fwd(cube, mode, h1, fc2, group, y, &S.fc2_lin, false, e2, s, fc2_pre);
 }
 
 void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSaved& S,
-             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s) {
+             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s,
+             const Operand* fc1_wg, const Operand* fc2_wg, const LinearSinks* fc1_sinks,
+             const LinearSinks* fc2_sinks) {
   // mlp_bwd (cube3d/transformer.hpp:55-70); GELU' fused into the FC2 dX epilogue.
   const int dt = dy.dtype;
   const ActGeom hg = act_geom(cube.grid(), dy.batch, dy.seq, 4 * cfg.hidden, 1 - dy.group);
@@ -468,58 +497,184 @@ void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSa
   Act dh1;
   dh1.data = dh.get();
   dh1.dtype = dt;
-  linear_bwd(cube, mode, dy, S.fc2_lin, fc2, &dh1, &g.w_fc2, &g.b_fc2, S.pre_act, s);
-  linear_bwd(cube, mode, dh1, S.fc1_lin, fc1, &dx, &g.w_fc1, &g.b_fc1, nullptr, s);
+  linear_bwd(cube, mode, dy, S.fc2_lin, fc2, &dh1, &g.w_fc2, &g.b_fc2, S.pre_act, s, fc2_wg,
+             fc2_sinks);
+  linear_bwd(cube, mode, dh1, S.fc1_lin, fc1, &dx, &g.w_fc1, &g.b_fc1, nullptr, s, fc1_wg,
+             fc1_sinks);
 }
 
 // ------------------------------------------------------------------- layer
+
+namespace {
+
+// The layer's four weights in one order: qkv, out, fc1, fc2.
+const Mat* layer_weights(const LayerP& p, int k) {
+  const Mat* w[4] = {&p.qkv.w, &p.out.w, &p.fc1.w, &p.fc2.w};
+  return w[k];
+}
+
+}  // namespace
 
 void layer_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LayerP& p, int& group,
                Act& y, LayerSaved* sv, cudaStream_t s) {
   // transformer_layer_fwd (cube3d/transformer.hpp:115-128):
   //   y1 = x + Attn(LN1(x)); y = y1 + MLP(LN2(y1)); residuals fused into the
   //   OUT and FC2 epilogues.
+  // Parameter collectives are hoisted and packed: every vector of the layer is
+  // expanded by one broadcast + one all-gather per direction triple, and the four
+  // weights by one all-gather along x; the backward reuses both (the reference
+  // re-gathers B in every matmul_ab_bwd, cube3d/ops3d.hpp:152).
   validate_config(cube, cfg);
   if (x.group != group) fail(C3D_ERR_GROUP_MISMATCH, "activation group does not match state");
   LayerSaved local;
   LayerSaved& S = sv ? *sv : local;
   const int dt = x.dtype;
   const size_t bytes = x.elems() * dtype_size(dt);
+  const int g = x.group;
+  bool packed_vecs = true;
+  for (const Vec* v : {&p.ln1_g, &p.ln1_b, &p.out.b, &p.ln2_g, &p.ln2_b, &p.fc2.b, &p.qkv.b,
+                       &p.fc1.b})
+    packed_vecs = packed_vecs && v->dtype == kF32;
+  LinearPre pre[4];
+  if (packed_vecs) {
+    S.keep(expand_diagonal_multi(cube, triple_for_group(g),
+                                 {p.ln1_g, p.ln1_b, p.out.b, p.ln2_g, p.ln2_b, p.fc2.b}, &S.vec0,
+                                 s));
+    S.keep(expand_diagonal_multi(cube, triple_for_group(1 - g), {p.qkv.b, p.fc1.b}, &S.vec1, s));
+    pre[0].bias = S.vec1[0];
+    pre[1].bias = S.vec0[2];
+    pre[2].bias = S.vec1[1];
+    pre[3].bias = S.vec0[5];
+  }
+  if (cube.extent(kX) > 1) {
+    bool same = true;
+    int64_t T = 0, off[4];
+    for (int k = 0; k < 4; ++k) {
+      off[k] = T;
+      T += static_cast<int64_t>(layer_weights(p, k)->elems());
+      same = same && layer_weights(p, k)->dtype == p.qkv.w.dtype;
+    }
+    if (same) {
+      const size_t es = dtype_size(p.qkv.w.dtype);
+      DevBuf send(static_cast<size_t>(T) * es, s);
+      for (int k = 0; k < 4; ++k)
+        C3D_CUDA(cudaMemcpyAsync(static_cast<char*>(send.get()) + off[k] * es,
+                                 layer_weights(p, k)->data, layer_weights(p, k)->elems() * es,
+                                 cudaMemcpyDeviceToDevice, s));
+      DevBuf& recv = S.keep(DevBuf(static_cast<size_t>(T) * cube.extent(kX) * es, s));
+      cube.all_gather(kX, send.get(), recv.get(), T, p.qkv.w.dtype, s);
+      for (int k = 0; k < 4; ++k) {
+        S.wg[k].ptr = static_cast<char*>(recv.get()) + off[k] * es;
+        S.wg[k].s_hi = T;
+        pre[k].wg = S.wg[k];
+      }
+    }
+  }
   Act n1;
   n1.data = S.keep(DevBuf(bytes, s)).get();
   n1.dtype = dt;
-  layernorm_fwd(cube, x, p.ln1_g, p.ln1_b, cfg.eps, n1, &S.ln1, s);
+  layernorm_fwd(cube, x, p.ln1_g, p.ln1_b, cfg.eps, n1, &S.ln1, s,
+                packed_vecs ? S.vec0[0] : nullptr, packed_vecs ? S.vec0[1] : nullptr);
   DevBuf y1buf(bytes, s);
   Act y1;
   y1.data = y1buf.get();
   y1.dtype = dt;
-  attention_fwd(cube, mode, cfg, n1, p.qkv, p.out, group, y1, &S.attn, false, x.data, s);
+  attention_fwd(cube, mode, cfg, n1, p.qkv, p.out, group, y1, &S.attn, false, x.data, s, &pre[0],
+                &pre[1]);
   Act n2;
   n2.data = S.keep(DevBuf(bytes, s)).get();
   n2.dtype = dt;
-  layernorm_fwd(cube, y1, p.ln2_g, p.ln2_b, cfg.eps, n2, &S.ln2, s);
-  mlp_fwd(cube, mode, cfg, n2, p.fc1, p.fc2, group, y, &S.mlp, false, y1.data, s);
+  layernorm_fwd(cube, y1, p.ln2_g, p.ln2_b, cfg.eps, n2, &S.ln2, s,
+                packed_vecs ? S.vec0[3] : nullptr, packed_vecs ? S.vec0[4] : nullptr);
+  mlp_fwd(cube, mode, cfg, n2, p.fc1, p.fc2, group, y, &S.mlp, false, y1.data, s, &pre[2],
+          &pre[3]);
 }
 
 void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const LayerSaved& S,
                const LayerP& p, Act& dx, LayerG& g, cudaStream_t s) {
-  // transformer_layer_bwd (cube3d/transformer.hpp:130-148)
+  // transformer_layer_bwd (cube3d/transformer.hpp:130-148). Vector-gradient column sums
+  // and weight-gradient partials are collected into packed buffers and reduced once
+  // per direction triple / once along x at the end.
   const int dt = dy.dtype;
   const size_t bytes = dy.elems() * dtype_size(dt);
+  const int grp = dy.group;
+  const Grid& grid = cube.grid();
+  const int64_t c0 = dy.cols;                                            // h / p_out(g)
+  const int64_t c1 = 3 * cfg.hidden / grid.dims[axis_of_group(grp)];     // 3h / p_out(1-g)
+  const int64_t c1b = 4 * cfg.hidden / grid.dims[axis_of_group(grp)];    // 4h / p_out(1-g)
+  // column-sum blocks: group-g triple [ln1 g|b, b_out, ln2 g|b, b_fc2], other [b_qkv, b_fc1]
+  DevBuf cs0(static_cast<size_t>(6 * c0) * sizeof(float), s);
+  DevBuf cs1(static_cast<size_t>(c1 + c1b) * sizeof(float), s);
+  float* f0 = cs0.as<float>();
+  float* f1 = cs1.as<float>();
+  LinearSinks sk[4];
+  sk[0].bias_colsum = f1;
+  sk[1].bias_colsum = f0 + 2 * c0;
+  sk[2].bias_colsum = f1 + c1;
+  sk[3].bias_colsum = f0 + 5 * c0;
+  // packed weight-gradient partials, reduce-scattered along x once
+  DevBuf dwpack;
+  const Mat* gw[4] = {&g.w_qkv, &g.w_out, &g.w_fc1, &g.w_fc2};
+  int64_t T = 0, off[4] = {0, 0, 0, 0};
+  const bool pack_dw = grid.dims[kX] > 1 && gw[0]->dtype == gw[1]->dtype &&
+                       gw[0]->dtype == gw[2]->dtype && gw[0]->dtype == gw[3]->dtype &&
+                       gw[0]->data && gw[1]->data && gw[2]->data && gw[3]->data;
+  if (pack_dw) {
+    for (int k = 0; k < 4; ++k) {
+      off[k] = T;
+      T += static_cast<int64_t>(layer_weights(p, k)->elems());
+    }
+    const size_t es = dtype_size(gw[0]->dtype);
+    dwpack = DevBuf(static_cast<size_t>(T) * grid.dims[kX] * es, s);
+    for (int k = 0; k < 4; ++k) {
+      sk[k].dw.base = static_cast<char*>(dwpack.get()) + off[k] * es;
+      sk[k].dw.s_hi = T;
+      sk[k].dw.dtype = gw[0]->dtype;
+    }
+  }
+  const Operand* wg[4];
+  for (int k = 0; k < 4; ++k) wg[k] = S.wg[k].ptr ? &S.wg[k] : nullptr;
+  const bool packed_vecs = !S.vec0.empty();
+  if (!packed_vecs)
+    for (auto& k : sk) k.bias_colsum = nullptr;  // each linear reduces its own bias grad
+
   DevBuf dn2b(bytes, s), dy1b(bytes, s), dn1b(bytes, s);
   Act dn2;
   dn2.data = dn2b.get();
   dn2.dtype = dt;
-  mlp_bwd(cube, mode, cfg, dy, S.mlp, p.fc1, p.fc2, dn2, g, s);
+  mlp_bwd(cube, mode, cfg, dy, S.mlp, p.fc1, p.fc2, dn2, g, s, wg[2], wg[3],
+          packed_vecs ? &sk[2] : (pack_dw ? &sk[2] : nullptr),
+          packed_vecs ? &sk[3] : (pack_dw ? &sk[3] : nullptr));
   Act dy1;
   dy1.data = dy1b.get();
   dy1.dtype = dt;
-  layernorm_bwd(cube, dn2, S.ln2, dy1, &g.ln2_g, &g.ln2_b, dy.data, s);  // dy1 = dy + LN2'
+  layernorm_bwd(cube, dn2, S.ln2, dy1, &g.ln2_g, &g.ln2_b, dy.data, s,
+                packed_vecs ? f0 + 3 * c0 : nullptr);  // dy1 = dy + LN2'
   Act dn1;
   dn1.data = dn1b.get();
   dn1.dtype = dt;
-  attention_bwd(cube, mode, cfg, dy1, S.attn, p.qkv, p.out, dn1, g, s);
-  layernorm_bwd(cube, dn1, S.ln1, dx, &g.ln1_g, &g.ln1_b, dy1.data, s);  // dx = dy1 + LN1'
+  attention_bwd(cube, mode, cfg, dy1, S.attn, p.qkv, p.out, dn1, g, s, wg[0], wg[1],
+                packed_vecs ? &sk[0] : (pack_dw ? &sk[0] : nullptr),
+                packed_vecs ? &sk[1] : (pack_dw ? &sk[1] : nullptr));
+  layernorm_bwd(cube, dn1, S.ln1, dx, &g.ln1_g, &g.ln1_b, dy1.data, s,
+                packed_vecs ? f0 : nullptr);  // dx = dy1 + LN1'
+  if (packed_vecs) {
+    Vec v0[6] = {g.ln1_g, g.ln1_b, g.b_out, g.ln2_g, g.ln2_b, g.b_fc2};
+    for (auto& v : v0) v.len = cfg.hidden;
+    Vec v1[2] = {g.b_qkv, g.b_fc1};
+    v1[0].len = 3 * cfg.hidden;
+    v1[1].len = 4 * cfg.hidden;
+    reduce_to_diagonal_multi(cube, triple_for_group(grp), f0, {v0, v0 + 6}, s);
+    reduce_to_diagonal_multi(cube, triple_for_group(1 - grp), f1, {v1, v1 + 2}, s);
+  }
+  if (pack_dw) {
+    const size_t es = dtype_size(gw[0]->dtype);
+    DevBuf mine(static_cast<size_t>(T) * es, s);
+    cube.reduce_scatter(kX, dwpack.get(), mine.get(), T, gw[0]->dtype, s);
+    for (int k = 0; k < 4; ++k)
+      C3D_CUDA(cudaMemcpyAsync(gw[k]->data, static_cast<char*>(mine.get()) + off[k] * es,
+                               layer_weights(p, k)->elems() * es, cudaMemcpyDeviceToDevice, s));
+  }
 }
 
 }  // namespace c3d

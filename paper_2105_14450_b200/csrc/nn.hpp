@@ -47,7 +47,21 @@ struct Saved {
 };
 
 struct LinearSaved : Saved {
-  Mat x;  // flattened forward input (LinearSaved::x_flat, cube3d/nn.hpp:69-72)
+  Mat x;           // flattened forward input (LinearSaved::x_flat, cube3d/nn.hpp:69-72)
+  Gathered a_full;  // the input as gathered by the forward (reused by the dW product)
+};
+
+// Layer-level precomputation handed to one linear: its bias already expanded and its
+// weight already gathered along x (one packed collective per layer for all of them).
+struct LinearPre {
+  const float* bias = nullptr;
+  Operand wg;
+};
+// Backward destinations for packed, deferred reductions: the bias column sums and the
+// un-reduced weight-gradient partial (reduced once per layer).
+struct LinearSinks {
+  float* bias_colsum = nullptr;
+  DwSink dw;
 };
 struct LNSaved : Saved {
   void* xhat = nullptr;
@@ -71,6 +85,10 @@ struct LayerSaved : Saved {
   LNSaved ln1, ln2;
   AttnSaved attn;
   MlpSaved mlp;
+  // expanded vectors (group-g triple: ln1 g/b, b_out, ln2 g/b, b_fc2; other triple:
+  // b_qkv, b_fc1) and the packed x-gathered weights, shared by forward and backward
+  std::vector<const float*> vec0, vec1;
+  Operand wg[4];  // qkv, out, fc1, fc2
 };
 
 struct LayerP {
@@ -95,26 +113,38 @@ struct LayerG {  // gradients (outputs), same shapes as LayerP
 // `own_input`: copy x into the saved state (standalone API); otherwise keep a view
 // (the caller guarantees x outlives backward, as inside a layer).
 void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group, Act& y,
-                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s);
+                LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s,
+                const LinearPre* pre = nullptr);
 void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, const LinearP& p,
-                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s);
+                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s,
+                const Operand* wg = nullptr, const LinearSinks* sinks = nullptr);
 
+// `gblock`/`bblock`: gamma/beta already expanded (layer-level); `colsum_sink`: write
+// [dgamma block | dbeta block] column sums there instead of reducing them here.
 void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, double eps,
-                   Act& y, LNSaved* saved, cudaStream_t s);
+                   Act& y, LNSaved* saved, cudaStream_t s, const float* gblock = nullptr,
+                   const float* bblock = nullptr);
 void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& saved, Act& dx, const Vec* dgamma,
-                   const Vec* dbeta, const void* resid, cudaStream_t s);
+                   const Vec* dbeta, const void* resid, cudaStream_t s,
+                   float* colsum_sink = nullptr);
 
 void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& qkv,
                    const LinearP& out, int& group, Act& y, AttnSaved* saved, bool own_input,
-                   const void* resid, cudaStream_t s);
+                   const void* resid, cudaStream_t s, const LinearPre* qkv_pre = nullptr,
+                   const LinearPre* out_pre = nullptr);
 void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const AttnSaved& sv,
-                   const LinearP& qkv, const LinearP& out, Act& dx, LayerG& g, cudaStream_t s);
+                   const LinearP& qkv, const LinearP& out, Act& dx, LayerG& g, cudaStream_t s,
+                   const Operand* qkv_wg = nullptr, const Operand* out_wg = nullptr,
+                   const LinearSinks* qkv_sinks = nullptr, const LinearSinks* out_sinks = nullptr);
 
 void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& fc1,
              const LinearP& fc2, int& group, Act& y, MlpSaved* saved, bool own_input,
-             const void* resid, cudaStream_t s);
+             const void* resid, cudaStream_t s, const LinearPre* fc1_pre = nullptr,
+             const LinearPre* fc2_pre = nullptr);
 void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSaved& sv,
-             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s);
+             const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s,
+             const Operand* fc1_wg = nullptr, const Operand* fc2_wg = nullptr,
+             const LinearSinks* fc1_sinks = nullptr, const LinearSinks* fc2_sinks = nullptr);
 
 void layer_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LayerP& p, int& group,
                Act& y, LayerSaved* saved, cudaStream_t s);

@@ -54,10 +54,31 @@ Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype
 // expand_diagonal (cube3d/ops3d.hpp:291-310): fp32 column block of length len/p_out
 // for an operand with triple d. Returns a stream-ordered fp32 buffer.
 DevBuf expand_diagonal(Cube& cube, const Dirs& d, const Vec& v, cudaStream_t s);
+// Several vectors sharing triple d in one broadcast + one all-gather: the result holds
+// their fp32 column blocks back to back; blocks[k] points at vector k's block.
+DevBuf expand_diagonal_multi(Cube& cube, const Dirs& d, const std::vector<Vec>& vs,
+                             std::vector<const float*>* blocks, cudaStream_t s);
 // reduce_to_diagonal (cube3d/ops3d.hpp:315-336) of `nvec` packed fp32 column-sum vectors
 // (each of length len/p_out) into the vectors out[0..nvec) on holder ranks.
 void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nvec,
                         const Vec* outs, cudaStream_t s);
+// Same for vectors of different lengths: colsums holds their column-sum blocks
+// (len_k / p_out each) back to back; one reduce-scatter + one all-reduce in total.
+void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
+                              const std::vector<Vec>& outs, cudaStream_t s);
+
+// An operand already gathered along its axis: [P][shard] blocks `s_hi` elements apart.
+struct Operand {
+  const void* ptr = nullptr;
+  long long s_hi = 0;
+};
+// Destination of an un-reduced weight-gradient partial inside a packed buffer that is
+// reduce-scattered along x once for all weights: column-block-major, blocks s_hi apart.
+struct DwSink {
+  void* base = nullptr;
+  long long s_hi = 0;
+  int dtype = kF32;
+};
 
 void matmul_ab_fwd(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, cudaStream_t s);
 void matmul_ab_bwd(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat& da,
@@ -83,11 +104,16 @@ struct LinearEpi {
   void* pre_act = nullptr;      // stores pre-activation (C layout)
   const void* resid = nullptr;  // C layout, C dtype
 };
+// `bg`: B already gathered along x (skips the gather). `keep_a`: receives the gathered A
+// (the caller keeps it for the backward instead of re-gathering, cube3d/ops3d.hpp:160).
 void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& epi,
-                cudaStream_t s);
+                cudaStream_t s, const Operand* bg = nullptr, Gathered* keep_a = nullptr);
 // dA = dC B^T (RS along d.in), dB = A^T dC (RS along x); either output may be skipped
 // (data == nullptr). `da_epi_aux`: if set, dA *= gelu'(aux) is fused (aux in dA layout).
+// `bg` / `ag`: pre-gathered B (along x) / A (along d.in). `dw`: write the dB partial into
+// a packed sink instead of reduce-scattering it here.
 void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
-                 Mat* db, const void* da_gelu_aux, cudaStream_t s);
+                 Mat* db, const void* da_gelu_aux, cudaStream_t s, const Operand* bg = nullptr,
+                 const void* ag = nullptr, const DwSink* dw = nullptr);
 
 }  // namespace c3d

@@ -185,6 +185,82 @@ void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nve
       k_convert(slice.as<float>() + k * n2, kF32, outs[k].data, outs[k].dtype, n2, s);
 }
 
+DevBuf expand_diagonal_multi(Cube& cube, const Dirs& d, const std::vector<Vec>& vs,
+                             std::vector<const float*>* blocks, cudaStream_t s) {
+  const Grid& g = cube.grid();
+  const int px = g.dims[kX];
+  if (g.dims[d.in] != g.dims[d.out])
+    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need equal input/output axis extents");
+  const bool holder = diagonal_holder(cube.coords());
+  std::vector<int64_t> n2(vs.size()), off(vs.size());
+  int64_t S = 0;
+  for (size_t k = 0; k < vs.size(); ++k) {
+    n2[k] = diagonal_slice(g, cube.coords(), vs[k].len).size();
+    off[k] = S;
+    S += n2[k];
+    if (vs[k].dtype != kF32) fail(C3D_ERR_CONFIG_INVALID, "packed expansion needs fp32 vectors");
+    if (holder && vs[k].data == nullptr)
+      fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
+  }
+  DevBuf out(static_cast<size_t>(S * px) * sizeof(float), s);
+  blocks->assign(vs.size(), nullptr);
+  for (size_t k = 0; k < vs.size(); ++k) (*blocks)[k] = out.as<float>() + off[k] * px;
+  if (g.size() == 1) {
+    for (size_t k = 0; k < vs.size(); ++k)
+      C3D_CUDA(cudaMemcpyAsync(out.as<float>() + off[k], vs[k].data, n2[k] * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s));
+    return out;
+  }
+  // holders pack their slices back to back, one broadcast along d.in, one gather along x
+  DevBuf piece(static_cast<size_t>(S) * sizeof(float), s);
+  if (holder)
+    for (size_t k = 0; k < vs.size(); ++k)
+      C3D_CUDA(cudaMemcpyAsync(piece.as<float>() + off[k], vs[k].data, n2[k] * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s));
+  cube.broadcast(d.in, cube.coord(d.out), piece.get(), S, kF32, s);
+  DevBuf full(static_cast<size_t>(S * px) * sizeof(float), s);
+  cube.all_gather(kX, piece.get(), full.get(), S, kF32, s);
+  // [q][k slice] -> per-vector column blocks [k][q slice]
+  for (size_t k = 0; k < vs.size(); ++k)
+    C3D_CUDA(cudaMemcpy2DAsync(out.as<float>() + off[k] * px, n2[k] * sizeof(float),
+                               full.as<float>() + off[k], S * sizeof(float),
+                               n2[k] * sizeof(float), px, cudaMemcpyDeviceToDevice, s));
+  return out;
+}
+
+void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
+                              const std::vector<Vec>& outs, cudaStream_t s) {
+  const Grid& g = cube.grid();
+  const int px = g.dims[kX];
+  const bool holder = diagonal_holder(cube.coords());
+  std::vector<int64_t> n2(outs.size()), off(outs.size());
+  int64_t S = 0;
+  for (size_t k = 0; k < outs.size(); ++k) {
+    n2[k] = diagonal_slice(g, cube.coords(), outs[k].len).size();
+    off[k] = S;
+    S += n2[k];
+    if (holder && outs[k].data == nullptr)
+      fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
+  }
+  if (g.size() == 1) {
+    for (size_t k = 0; k < outs.size(); ++k)
+      k_convert(colsums + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
+    return;
+  }
+  // column-sum blocks [k][q slice] -> position-major [q][k slice] for the reduce-scatter
+  DevBuf packed(static_cast<size_t>(S * px) * sizeof(float), s);
+  for (size_t k = 0; k < outs.size(); ++k)
+    C3D_CUDA(cudaMemcpy2DAsync(packed.as<float>() + off[k], S * sizeof(float),
+                               colsums + off[k] * px, n2[k] * sizeof(float),
+                               n2[k] * sizeof(float), px, cudaMemcpyDeviceToDevice, s));
+  DevBuf slice(static_cast<size_t>(S) * sizeof(float), s);
+  cube.reduce_scatter(kX, packed.get(), slice.get(), S, kF32, s);
+  cube.all_reduce(d.in, slice.get(), S, kF32, false, s);
+  if (holder)
+    for (size_t k = 0; k < outs.size(); ++k)
+      k_convert(slice.as<float>() + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
+}
+
 void add_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s) {
   require_input_family(a, "A");
   if (b.len != a.gcols)
@@ -235,19 +311,27 @@ void mul_vec_bwd(Cube& cube, const Mat& dc, const Mat& a, const Vec& b, Mat& da,
 // ---------------------------------------------------------------- C = A B
 
 void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& le,
-                cudaStream_t s) {
+                cudaStream_t s, const Operand* bg, Gathered* keep_a) {
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // a: (M/(Pw Pin)) x (N/Pout); b: (N/Pout) x (K/(Pin Pw))
   Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
-  Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);   // [Pw][N/Pout][K/(Pin Pw)]
+  Gathered bf;
+  long long b_hi = b.rows * b.cols;
+  if (bg && bg->ptr) {
+    bf.ptr = bg->ptr;
+    b_hi = bg->s_hi;
+  } else {
+    bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);  // [Pw][N/Pout][K/(Pin Pw)]
+  }
   const int64_t Mg = a.rows * Pin, Kg = a.cols, Ng = b.cols * Pw;
   View av = kmajor(af.ptr, a.dtype, a.cols);
   View bv = mnmajor(bf.ptr, b.dtype, b.cols);
   if (Pw > 1) {
     bv.rsplit = b.cols;
-    bv.s_hi = b.rows * b.cols;
+    bv.s_hi = b_hi;
   }
+  if (keep_a) *keep_a = std::move(af);  // buffer (if any) outlives this call
   c = make_mat(cube, c.data, c.dtype, a.grows, b.gcols, kOutput, d.swapped());
   Epilogue e;
   if (Pout == 1) {
@@ -279,21 +363,29 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
 }
 
 void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
-                 Mat* db, const void* da_gelu_aux, cudaStream_t s) {
+                 Mat* db, const void* da_gelu_aux, cudaStream_t s, const Operand* bg,
+                 const void* ag, const DwSink* dw) {
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // dC: (M/(Pw Pout)) x (K/Pin) with triple d.swapped(): gather along d.out
   Gathered dcf = gather(cube, d.out, dc.data, dc.elems(), dc.dtype, s);  // (M/Pw) x (K/Pin)
   const int64_t Mrows = dc.rows * Pout, Kc = dc.cols;
   if (da && da->data) {
-    Gathered bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);
+    Gathered bf;
+    long long b_hi = b.rows * b.cols;
+    if (bg && bg->ptr) {
+      bf.ptr = bg->ptr;
+      b_hi = bg->s_hi;
+    } else {
+      bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);
+    }
     *da = make_mat(cube, da->data, da->dtype, a.grows, a.gcols, a.layout, a.dirs);
     // partial dA (M/Pw) x (N/Pout) = dc_full * b_full^T
     View av = kmajor(dcf.ptr, dc.dtype, Kc);
     View bv = kmajor(bf.ptr, b.dtype, b.cols);
     if (Pw > 1) {
       bv.csplit = b.cols;
-      bv.s_hi = b.rows * b.cols;
+      bv.s_hi = b_hi;
     }
     Epilogue e;
     if (Pin == 1) {
@@ -320,7 +412,9 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
     }
   }
   if (db && db->data) {
-    Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+    Gathered af;
+    if (ag) af.ptr = ag;
+    else af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
     *db = make_mat(cube, db->data, db->dtype, b.grows, b.gcols, kWeight, d);
     // partial dB[k_in][n] = sum_m a_full[m][k_in] dc_full[m][n], written column-block-major
     // [Pw][N/Pout][K/(Pin Pw)] so the reduce-scatter along x lands each rank's shard.
@@ -329,6 +423,11 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
     Epilogue e;
     if (Pw == 1) {
       e.out = out_view(db->data, db->dtype, db->cols);
+      local_gemm(cube, mode, a.cols, Kc, Mrows, av, bv, e, s);
+    } else if (dw && dw->base) {
+      e.out = out_view(dw->base, dw->dtype, db->cols);
+      e.out.csplit = db->cols;
+      e.out.s_hi = dw->s_hi;
       local_gemm(cube, mode, a.cols, Kc, Mrows, av, bv, e, s);
     } else {
       DevBuf partial(static_cast<size_t>(a.cols * Kc) * dtype_size(db->dtype), s);
