@@ -288,6 +288,7 @@ def our_arm(args, wl):
         step(x, dy)
     torch.cuda.synchronize()
     gemm_ms, gemm_flops, gemm_n = c3.prof_read()
+    comm_ms, comm_bytes, comm_n = c3.prof_read_comm()
     c3.prof_enable(False)
 
     # ---- end-to-end through the public API with host buffers (H2D + D2H inside)
@@ -380,6 +381,11 @@ def our_arm(args, wl):
                                    f"{args.steps} eager steps"},
             "layer_tflops": layer_tflops,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
+            "collectives": {"calls_per_step": comm_n / args.steps,
+                            "ms_per_step": comm_ms / args.steps,
+                            "payload_mb_per_step": comm_bytes / args.steps / 1e6,
+                            "timing": "per-call CUDA events on the issuing stream, rank 0, "
+                                      "eager steps"},
             "clocks": clk,
             "cpu_baseline": cpu,
         }

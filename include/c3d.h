@@ -90,6 +90,9 @@ long long c3d_launch_count(void);
  * summed algorithmic flops (2*M*N*K*batch) and launch count, then resets. */
 int c3d_prof_enable(int on);
 int c3d_prof_read(double* ms, double* flops, long long* launches);
+/* Same for the collectives recorded since c3d_prof_enable: summed per-call time (ms),
+ * summed payload bytes (full gathered / pre-scatter buffer) and call count. */
+int c3d_prof_read_comm(double* ms, double* bytes, long long* calls);
 
 /* ------------------------------------------------------ pure host: inputs */
 /* Rng (cube3d/rng.hpp:17-34): mt19937_64 with the reference's explicit 53-bit
@@ -160,6 +163,24 @@ int c3d_cube_info(const c3d_cube* cube, int* rank, int coords[3], int dims[3]);
 int c3d_cube_barrier(c3d_cube* cube, void* stream);
 int c3d_counters_get(const c3d_cube* cube, c3d_counters* out);
 int c3d_counters_reset(c3d_cube* cube);
+
+/* Endpoint collectives along one axis line (cube3d/transport.hpp:160-257), device
+ * buffers, stream-ordered, charged to the counters like the reference. Counts are in
+ * elements of `dtype`. Positions ascend along the axis; reductions sum (or max) in
+ * ascending position order. Transport: peer-memory push kernels over NVLink
+ * (NCCL when C3D_NCCL_COLL=1).
+ *   broadcast:      buf[count] from the rank at `root_position`   (:160-184)
+ *   all_gather:     send[count] -> recv[p][count]                 (:188-203)
+ *   reduce_scatter: send[p][count] -> recv[count] (own position)  (:208-232)
+ *   all_reduce:     buf[count] in place, op 0 = sum, 1 = max      (:236-257) */
+int c3d_broadcast(c3d_cube* cube, int axis, int root_position, void* buf, size_t count,
+                  int dtype, void* stream);
+int c3d_all_gather(c3d_cube* cube, int axis, const void* send, void* recv, size_t count,
+                   int dtype, void* stream);
+int c3d_reduce_scatter(c3d_cube* cube, int axis, const void* send, void* recv, size_t count,
+                       int dtype, void* stream);
+int c3d_all_reduce(c3d_cube* cube, int axis, void* buf, size_t count, int dtype, int op,
+                   void* stream);
 
 /* ------------------------------------------------------------- tensors */
 /* ShardedMatrix (cube3d/sharding.hpp:18-34): the local shard is a dense row-major

@@ -83,6 +83,7 @@ SIGNATURES = {
     "c3d_launch_count": [],
     "c3d_prof_enable": [C.c_int],
     "c3d_prof_read": [P(C.c_double), P(C.c_double), P(C.c_longlong)],
+    "c3d_prof_read_comm": [P(C.c_double), P(C.c_double), P(C.c_longlong)],
     "c3d_rng_create": [C.c_uint64, P(VP)],
     "c3d_rng_destroy": [VP],
     "c3d_rng_next_u64": [VP, P(C.c_uint64), C.c_int64],
@@ -104,6 +105,10 @@ SIGNATURES = {
     "c3d_cube_barrier": [VP, VP],
     "c3d_counters_get": [VP, P(c3d_counters)],
     "c3d_counters_reset": [VP],
+    "c3d_broadcast": [VP, C.c_int, C.c_int, VP, C.c_size_t, C.c_int, VP],
+    "c3d_all_gather": [VP, C.c_int, VP, VP, C.c_size_t, C.c_int, VP],
+    "c3d_reduce_scatter": [VP, C.c_int, VP, VP, C.c_size_t, C.c_int, VP],
+    "c3d_all_reduce": [VP, C.c_int, VP, C.c_size_t, C.c_int, C.c_int, VP],
     "c3d_gemm": [C.c_int64, C.c_int64, C.c_int64, C.c_int, P(c3d_view), P(c3d_view),
                  P(c3d_view), C.c_float, VP, C.c_int, C.c_int, C.c_int, VP],
     "c3d_matmul_ab_fwd": [VP, C.c_int, P(c3d_matrix), P(c3d_matrix), P(c3d_matrix), VP],

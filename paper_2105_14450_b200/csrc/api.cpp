@@ -184,6 +184,9 @@ int c3d_prof_enable(int on) {
 int c3d_prof_read(double* ms, double* flops, long long* launches) {
   return guard([&] { c3d::prof_read(ms, flops, launches); });
 }
+int c3d_prof_read_comm(double* ms, double* bytes, long long* calls) {
+  return guard([&] { c3d::prof_read_comm(ms, bytes, calls); });
+}
 
 // ---------------------------------------------------------------- rng
 int c3d_rng_create(uint64_t seed, c3d_rng** out) {
@@ -347,6 +350,44 @@ int c3d_counters_get(const c3d_cube* cube, c3d_counters* out) {
 }
 int c3d_counters_reset(c3d_cube* cube) {
   return guard([&] { get(cube).reset_counters(); });
+}
+
+namespace {
+void check_axis_dtype(int axis, int dtype) {
+  if (axis < 0 || axis > 2) c3d::fail(C3D_ERR_OUT_OF_RANGE, "axis " + std::to_string(axis));
+  if (dtype != C3D_F32 && dtype != C3D_BF16)
+    c3d::fail(C3D_ERR_CONFIG_INVALID, "dtype " + std::to_string(dtype));
+}
+}  // namespace
+
+int c3d_broadcast(c3d_cube* cube, int axis, int root_position, void* buf, size_t count,
+                  int dtype, void* stream) {
+  return guard([&] {
+    check_axis_dtype(axis, dtype);
+    get(cube).broadcast(axis, root_position, buf, count, dtype, as_stream(stream));
+  });
+}
+int c3d_all_gather(c3d_cube* cube, int axis, const void* send, void* recv, size_t count,
+                   int dtype, void* stream) {
+  return guard([&] {
+    check_axis_dtype(axis, dtype);
+    get(cube).all_gather(axis, send, recv, count, dtype, as_stream(stream));
+  });
+}
+int c3d_reduce_scatter(c3d_cube* cube, int axis, const void* send, void* recv, size_t count,
+                       int dtype, void* stream) {
+  return guard([&] {
+    check_axis_dtype(axis, dtype);
+    get(cube).reduce_scatter(axis, send, recv, count, dtype, as_stream(stream));
+  });
+}
+int c3d_all_reduce(c3d_cube* cube, int axis, void* buf, size_t count, int dtype, int op,
+                   void* stream) {
+  return guard([&] {
+    check_axis_dtype(axis, dtype);
+    if (op != 0 && op != 1) c3d::fail(C3D_ERR_CONFIG_INVALID, "all_reduce op must be 0 or 1");
+    get(cube).all_reduce(axis, buf, count, dtype, op == 1, as_stream(stream));
+  });
 }
 
 // ---------------------------------------------------------------- GEMM

@@ -17,6 +17,21 @@ void nccl_check(ncclResult_t r, const char* what) {
     fail(C3D_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
+// Brackets one collective with profiler events when profiling is on. `bytes` is the
+// full (gathered / pre-scatter) payload.
+struct Timed {
+  cudaStream_t s;
+  void* tok = nullptr;
+  int tag;
+  double bytes;
+  Timed(cudaStream_t st, int kind, double b) : s(st), tag(kind), bytes(b) {
+    if (prof_on()) prof_begin(s, &tok);
+  }
+  ~Timed() {
+    if (tok) prof_end(s, tok, tag, bytes);
+  }
+};
+
 }  // namespace
 
 Cube::Cube(const int dims[3], int rank, int device, const unsigned char* uid)
@@ -41,10 +56,28 @@ Cube::Cube(const int dims[3], int rank, int device, const unsigned char* uid)
       nccl_check(ncclCommSplit(world_, color, coords_[a], &axis_comm_[a], nullptr),
                  "ncclCommSplit");
     }
+    if (std::getenv("C3D_NCCL_COLL") == nullptr) {
+      const char* mb = std::getenv("C3D_MAILBOX_MB");
+      const size_t bytes = static_cast<size_t>(mb ? std::atol(mb) : 256) << 20;
+      const char* ab = std::getenv("C3D_ARENA_MB");
+      const size_t arena = static_cast<size_t>(ab ? std::atol(ab) : 512) << 20;
+      symm_ = std::make_unique<SymmHeap>(world_, grid_.size(), rank, bytes, arena, nullptr);
+    }
+  }
+  for (int a = 0; a < 3; ++a) line_[a] = grid_.axis_group(coords_, a);
+  if (symm_) {
+    C3D_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    C3D_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
+    C3D_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
   }
 }
 
 Cube::~Cube() {
+  if (side_) cudaStreamSynchronize(side_);
+  symm_.reset();
+  if (fork_) cudaEventDestroy(fork_);
+  if (join_) cudaEventDestroy(join_);
+  if (side_) cudaStreamDestroy(side_);
   for (auto& c : axis_comm_)
     if (c) ncclCommDestroy(c);
   if (world_) ncclCommDestroy(world_);
@@ -91,7 +124,12 @@ void Cube::all_gather(int axis, const void* send, void* recv, size_t count, int 
       C3D_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dtype), cudaMemcpyDeviceToDevice, s));
     return;
   }
-  nccl_check(ncclAllGather(send, recv, count, nccl_type(dtype), comm(axis), s), "ncclAllGather");
+  Timed t(s, C3D_ALL_GATHER, static_cast<double>(p) * count * dtype_size(dtype));
+  if (symm_)
+    symm_->collective(kCollAllGather, line_[axis], coords_[axis], send, recv, count, dtype, 0,
+                      false, num_sms_, s);
+  else
+    nccl_check(ncclAllGather(send, recv, count, nccl_type(dtype), comm(axis), s), "ncclAllGather");
   charge(C3D_ALL_GATHER, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
 }
 
@@ -103,8 +141,13 @@ void Cube::reduce_scatter(int axis, const void* send, void* recv, size_t count, 
       C3D_CUDA(cudaMemcpyAsync(recv, send, count * dtype_size(dtype), cudaMemcpyDeviceToDevice, s));
     return;
   }
-  nccl_check(ncclReduceScatter(send, recv, count, nccl_type(dtype), ncclSum, comm(axis), s),
-             "ncclReduceScatter");
+  Timed t(s, C3D_REDUCE_SCATTER, static_cast<double>(p) * count * dtype_size(dtype));
+  if (symm_)
+    symm_->collective(kCollReduceScatter, line_[axis], coords_[axis], send, recv, count, dtype, 0,
+                      false, num_sms_, s);
+  else
+    nccl_check(ncclReduceScatter(send, recv, count, nccl_type(dtype), ncclSum, comm(axis), s),
+               "ncclReduceScatter");
   charge(C3D_REDUCE_SCATTER, static_cast<uint64_t>(p - 1) * count,
          static_cast<uint64_t>(p - 1) * count);
 }
@@ -112,9 +155,14 @@ void Cube::reduce_scatter(int axis, const void* send, void* recv, size_t count, 
 void Cube::all_reduce(int axis, void* buf, size_t count, int dtype, bool is_max, cudaStream_t s) {
   const int p = extent(axis);
   if (p == 1) return;
-  nccl_check(ncclAllReduce(buf, buf, count, nccl_type(dtype), is_max ? ncclMax : ncclSum,
-                           comm(axis), s),
-             "ncclAllReduce");
+  Timed t(s, C3D_ALL_REDUCE, static_cast<double>(count) * dtype_size(dtype));
+  if (symm_)
+    symm_->collective(kCollAllReduce, line_[axis], coords_[axis], buf, buf, count, dtype, 0,
+                      is_max, num_sms_, s);
+  else
+    nccl_check(ncclAllReduce(buf, buf, count, nccl_type(dtype), is_max ? ncclMax : ncclSum,
+                             comm(axis), s),
+               "ncclAllReduce");
   charge(C3D_ALL_REDUCE, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
 }
 
@@ -124,8 +172,13 @@ void Cube::broadcast(int axis, int root_position, void* buf, size_t count, int d
   if (root_position < 0 || root_position >= p)
     fail(C3D_ERR_OUT_OF_RANGE, "broadcast root position " + std::to_string(root_position));
   if (p == 1) return;
-  nccl_check(ncclBroadcast(buf, buf, count, nccl_type(dtype), root_position, comm(axis), s),
-             "ncclBroadcast");
+  Timed t(s, C3D_BROADCAST, static_cast<double>(count) * dtype_size(dtype));
+  if (symm_)
+    symm_->collective(kCollBroadcast, line_[axis], coords_[axis], buf, buf, count, dtype,
+                      root_position, false, num_sms_, s);
+  else
+    nccl_check(ncclBroadcast(buf, buf, count, nccl_type(dtype), root_position, comm(axis), s),
+               "ncclBroadcast");
   if (coords_[axis] == root_position)
     charge(C3D_BROADCAST, static_cast<uint64_t>(p - 1) * count, 0);
   else

@@ -16,15 +16,23 @@
 #include <array>
 #include <cstddef>
 #include <cstring>
+#include <memory>
 #include <string>
+#include <vector>
 
 #include "common.hpp"
 #include "gemm.hpp"
 #include "grid.hpp"
+#include "symm.hpp"
 
 namespace c3d {
 
 size_t dtype_size(int dtype);
+
+// Event brackets for collectives (profiler in gemm_dispatch.cpp; no-ops when disabled).
+bool prof_on();
+void prof_begin(cudaStream_t s, void** token);
+void prof_end(cudaStream_t s, void* token, int tag, double bytes);
 
 // Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
 class DevBuf {
@@ -79,6 +87,13 @@ class Cube {
   int extent(int axis) const { return grid_.dims[axis]; }
   int device() const { return device_; }
   int num_sms() const { return num_sms_; }
+  // Peer-memory transport, or null when collectives go through NCCL (C3D_NCCL_COLL=1).
+  SymmHeap* symm() const { return symm_.get(); }
+  const std::vector<int>& line(int axis) const { return line_[axis]; }
+  // Second stream (copy-engine pushes overlapping the main stream) and fork/join events.
+  cudaStream_t side_stream() const { return side_; }
+  cudaEvent_t fork_event() const { return fork_; }
+  cudaEvent_t join_event() const { return join_; }
 
   // Collectives along one axis line. Counts are in elements.
   void all_gather(int axis, const void* send, void* recv, size_t count, int dtype,
@@ -90,6 +105,8 @@ class Cube {
   void broadcast(int axis, int root_position, void* buf, size_t count, int dtype, cudaStream_t s);
   void barrier(cudaStream_t s);
 
+  // Charges a transfer done outside the collectives above (fused operators).
+  void account(int kind, uint64_t sent, uint64_t received) { charge(kind, sent, received); }
   c3d_counters& counters() { return counters_; }
   const c3d_counters& counters() const { return counters_; }
   void add_madds(uint64_t n) { counters_.multiply_adds += n; }
@@ -106,6 +123,10 @@ class Cube {
   int num_sms_ = 148;
   ncclComm_t world_ = nullptr;
   ncclComm_t axis_comm_[3] = {nullptr, nullptr, nullptr};
+  std::unique_ptr<SymmHeap> symm_;  // peer-memory transport (null: NCCL for everything)
+  std::vector<int> line_[3];        // world ranks of this rank's axis lines, by position
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   c3d_counters counters_{};
 };
 

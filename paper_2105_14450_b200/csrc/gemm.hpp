@@ -66,11 +66,48 @@ struct Epilogue {
   int accumulate = 0;
 };
 
+// Reduce-scatter fused into the tcgen05 GEMM epilogue: C's rows form P blocks of
+// block_rows; block k is TMA-stored to dst[k] ([block_rows][N] row-major), which for
+// k != me is this rank's slot in rank k's symmetric receive buffer over NVLink. Before
+// its first store to block k a CTA waits for k's entry flag; after its last store it
+// raises done[k][blockIdx.x] to the epoch (release, system scope).
+constexpr int kRsMax = 4;
+struct RsOut {
+  int P = 0;  // 0: plain GEMM
+  int me = 0;
+  int block0 = 0;       // block index of the GEMM's first row (row-split launches)
+  int done_offset = 0;  // first done-flag slot of this launch
+  long long block_rows = 0;
+  void* dst[kRsMax] = {};
+  const uint32_t* entered[kRsMax] = {};
+  uint32_t* done[kRsMax] = {};
+  const uint32_t* epoch = nullptr;
+};
+
+// All-gather fused into the GEMM (lines of 2, with a fused reduce-scatter whose epoch it
+// shares): A's rows form 2 blocks of block_rows, block k read from a_block[k]
+// ([block_rows][K] K-major bf16; a_block[own] is this rank's shard). A dedicated warp
+// per CTA pushes 1/grid of the shard to push_dst (this rank's slot in the peer's
+// gathered buffer) and own_dst (optional local copy), then raises signal[cta]. Own-block
+// tiles are scheduled first; before loading the other block the TMA producer waits
+// for every peer CTA's flag in wait[].
+struct AgIn {
+  long long block_rows = 0;  // 0: plain operand A
+  int own = 0;
+  const void* a_block[2] = {};
+  void* push_dst = nullptr;
+  void* own_dst = nullptr;
+  uint32_t* signal = nullptr;
+  const uint32_t* wait = nullptr;
+};
+
 struct GemmProblem {
   long long M = 0, N = 0, K = 0;
   int batch = 1;
   View a, b;  // a: [batch][M][K], b: [batch][N][K]
   Epilogue epi;
+  RsOut rs;
+  AgIn ag;
 };
 
 }  // namespace c3d

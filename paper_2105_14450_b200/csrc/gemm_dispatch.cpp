@@ -1,6 +1,8 @@
 // Chooses the tcgen05 or SIMT kernel for one local product, and (when enabled)
 // brackets every tcgen05 launch with CUDA events on its stream so bench.py can
 // report the dominant kernel's achieved TFLOP/s from the live run.
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -15,7 +17,9 @@ namespace {
 
 struct ProfRec {
   cudaEvent_t start, stop;
-  double flops;
+  double flops;  // GEMM flops, or collective payload bytes
+  int kind;      // 0 = tcgen05 GEMM, 1 = collective
+  int tag;       // collective kind (C3D_BROADCAST ...)
 };
 
 struct Profiler {
@@ -49,22 +53,71 @@ void prof_enable(bool on) {
   prof().next = 0;
 }
 
-// Returns (sum of per-launch ms, sum of flops, launches) and resets the log.
-void prof_read(double* ms, double* flops, long long* launches) {
-  std::lock_guard<std::mutex> g(prof().mu);
+namespace {
+// Sums the records of one kind and drops them (the event pool is recycled once the log
+// is empty). C3D_PROF_DUMP prints every collective record.
+void read_kind(int kind, double* ms, double* amount, long long* count) {
+  Profiler& pr = prof();
+  std::lock_guard<std::mutex> g(pr.mu);
+  static const bool dump = std::getenv("C3D_PROF_DUMP") != nullptr;
   double t = 0, f = 0;
-  for (auto& r : prof().recs) {
+  long long n = 0;
+  std::vector<ProfRec> rest;
+  for (auto& r : pr.recs) {
+    if (r.kind != kind) {
+      rest.push_back(r);
+      continue;
+    }
     C3D_CUDA(cudaEventSynchronize(r.stop));
     float x = 0;
     C3D_CUDA(cudaEventElapsedTime(&x, r.start, r.stop));
+    if (dump && kind == 1)
+      std::fprintf(stderr, "[c3d prof] coll kind=%d bytes=%.0f us=%.1f GB/s=%.1f\n", r.tag, r.flops,
+                   1e3 * x, x > 0 ? r.flops / (x * 1e6) : 0.0);
+    if (kind == 1 && r.tag >= 5) continue;  // fused-operator spans: dumped, not summed
     t += x;
     f += r.flops;
+    ++n;
   }
   *ms = t;
-  *flops = f;
-  *launches = static_cast<long long>(prof().recs.size());
-  prof().recs.clear();
-  prof().next = 0;
+  *amount = f;
+  *count = n;
+  pr.recs.swap(rest);
+  if (pr.recs.empty()) pr.next = 0;
+}
+}  // namespace
+
+// Returns (sum of per-launch ms, sum of flops, launches) of the tcgen05 GEMMs.
+void prof_read(double* ms, double* flops, long long* launches) {
+  read_kind(0, ms, flops, launches);
+}
+
+// Returns (sum of per-call ms, sum of payload bytes, calls) of the collectives.
+void prof_read_comm(double* ms, double* bytes, long long* calls) {
+  read_kind(1, ms, bytes, calls);
+}
+
+bool prof_on() { return prof().enabled; }
+
+void prof_begin(cudaStream_t s, void** token) {
+  Profiler& pr = prof();
+  std::lock_guard<std::mutex> g(pr.mu);
+  cudaEvent_t e = pr.take();
+  C3D_CUDA(cudaEventRecord(e, s));
+  *token = e;
+}
+
+void prof_end(cudaStream_t s, void* token, int tag, double bytes) {
+  Profiler& pr = prof();
+  std::lock_guard<std::mutex> g(pr.mu);
+  ProfRec rec{};
+  rec.start = static_cast<cudaEvent_t>(token);
+  rec.stop = pr.take();
+  rec.flops = bytes;
+  rec.kind = 1;
+  rec.tag = tag;
+  C3D_CUDA(cudaEventRecord(rec.stop, s));
+  pr.recs.push_back(rec);
 }
 
 void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s) {
@@ -81,6 +134,7 @@ void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s) {
         rec.start = pr.take();
         rec.stop = pr.take();
         rec.flops = 2.0 * p.M * p.N * p.K * p.batch;
+        rec.kind = 0;
         C3D_CUDA(cudaEventRecord(rec.start, s));
       }
       tc_gemm_launch(p, bn, num_sms, s);

@@ -40,7 +40,8 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kCommWarp = 2 + kEpiWarps;  // pushes the all-gather shard (fused mode)
+constexpr int kThreads = 64 + 32 * kEpiWarps + 32;
 constexpr int kSmemBudget = 227 * 1024;
 
 struct TcOperand {
@@ -65,6 +66,25 @@ struct TcArgs {
   int st_blo;                // batch-lo extent of the stored view
   TcOperand a, b;
   Epilogue epi;
+  // fused reduce-scatter (rs_P > 1): block k of the rows goes through rsm.m[k]
+  int rs_P, rs_me, rs_block_rows, rs_block0, rs_done_offset;
+  const uint32_t* rs_entered[kRsMax];
+  uint32_t* rs_done[kRsMax];
+  const uint32_t* rs_epoch;
+  // fused all-gather (ag_rows > 0): A row block k through agm.m[k]; tiles rotated so the
+  // own block comes first; the other block waits for *ag_ready == 1
+  int ag_rows, ag_own, m_rot;
+  const char* ag_src;       // this rank's shard
+  char* ag_peer_dst;        // its slot in the peer's gathered buffer (NVLink mapping)
+  char* ag_own_dst;         // its slot in the local gathered buffer (null: not kept)
+  long long ag_bytes;
+  uint32_t* ag_signal;      // peer's arrival flags for this rank, [cta]
+  const uint32_t* ag_wait;  // this rank's arrival flags for the peer, [cta]
+};
+
+struct RsMaps {
+  CUtensorMap m[kRsMax];
+  CUtensorMap ag[2];
 };
 
 // Writes one 32-value row segment (CW = 32 fp32 or 64 bf16 values = 128 B) into row
@@ -165,9 +185,11 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
   const int per_batch = a.m_tiles * a.n_tiles;
   u.b = tile / per_batch;
   const int rem = tile - u.b * per_batch;
-  const int mt = rem / a.n_tiles;
+  const int mr = rem / a.n_tiles;
+  int mt = mr + a.m_rot;
+  if (mt >= a.m_tiles) mt -= a.m_tiles;
   u.m0 = mt * kBM;
-  u.n0 = (rem - mt * a.n_tiles) * bn;
+  u.n0 = (rem - mr * a.n_tiles) * bn;
   u.kb0 = u.ks * a.kb_per_split;
   u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
   return u;
@@ -370,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC,
-                   const __grid_constant__ CUtensorMap tmP, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap tmP, const TcArgs args,
+                   const __grid_constant__ RsMaps rsm) {
   constexpr int kABytes = kBM * kBK * 2;  // 16 KB
   constexpr int kBBytes = BN * kBK * 2;
   constexpr int kStageBytes = kABytes + kBBytes;
@@ -421,14 +444,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       OpPos pa, pb;
+      bool ag_ok = false;
       for (int t = blockIdx.x; t < units; t += gridDim.x) {
         const Unit u = decode_unit(args, t, BN);
-        op_init(args.a, pa, u.m0, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
+        const CUtensorMap* amap = &tmA;
+        int arow = u.m0;
+        if (args.ag_rows) {
+          const int blk = u.m0 / args.ag_rows;
+          amap = &rsm.ag[blk];
+          arow = u.m0 - blk * args.ag_rows;
+          if (blk != args.ag_own && !ag_ok) {
+            // the peer's comm warps (one per CTA) have pushed its rows
+            const uint32_t epoch = *args.rs_epoch;
+            for (int c = 0; c < static_cast<int>(gridDim.x); ++c) ptx::wait_epoch(args.ag_wait + c, epoch);
+            ptx::fence_proxy_async_global();
+            ag_ok = true;
+          }
+        }
+        op_init(args.a, pa, arow, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
         op_init(args.b, pb, u.n0, B_MN ? BN / 64 : 1, u.kb0 * kBK, u.b);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          op_issue<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
+          op_issue<kBM>(amap, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
           op_issue<BN>(&tmB, args.b, pb, smem_b + s * kBBytes, &full_bar[s]);
           op_advance(args.a, pa);
           op_advance(args.b, pb);
@@ -478,6 +516,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if (warp == kCommWarp) {
+    if (args.ag_rows) {
+      // ---------------- all-gather push: this CTA's 1/grid of the shard goes to the
+      // peer's gathered buffer over NVLink (and to the local one when it is kept), then
+      // a per-CTA arrival flag is raised on the peer (release, system scope)
+      constexpr int U = 8;
+      const long long nvec = args.ag_bytes / 16;
+      const long long lo = nvec * blockIdx.x / gridDim.x, hi = nvec * (blockIdx.x + 1) / gridDim.x;
+      const uint4* src = reinterpret_cast<const uint4*>(args.ag_src);
+      uint4* dst = reinterpret_cast<uint4*>(args.ag_peer_dst);
+      uint4* own = reinterpret_cast<uint4*>(args.ag_own_dst);
+      for (long long i0 = lo + lane; i0 < hi; i0 += 32 * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + 32 * u < hi) v[u] = src[i0 + 32 * u];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (i0 + 32 * u < hi) {
+            dst[i0 + 32 * u] = v[u];
+            if (own) own[i0 + 32 * u] = v[u];
+          }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        ptx::st_release_sys(args.ag_signal + blockIdx.x, *args.rs_epoch);
+      }
+    }
   } else {
     // ---------------- epilogue warps 2..9: lane quarter = warp % 4, column half = (warp-2)/4
     const int quarter = warp & 3;
@@ -489,6 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* buf = smem_stage + (warp - 2) * 4096;
       const bool need_off =
           args.ksplit == 1 && (e.aux != nullptr || e.resid != nullptr || e.accumulate);
+      const uint32_t epoch = args.rs_P ? *args.rs_epoch : 0u;
+      uint32_t entered_mask = 0;
       for (int t = blockIdx.x; t < units; t += gridDim.x) {
         const Unit u = decode_unit(args, t, BN);
         const int mrow0 = u.m0 + quarter * 32;
@@ -497,19 +566,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long row_off = (need_off && row_ok) ? view_offset(e.out, u.b, m, 0) : 0;
         const int bidx = args.ksplit > 1 ? u.ks : u.b;
         const int c3 = bidx % args.st_blo, c4 = bidx / args.st_blo;
-        const int c1 = args.st_rsplit ? mrow0 % args.st_rsplit : mrow0;
+        int c1 = args.st_rsplit ? mrow0 % args.st_rsplit : mrow0;
         const int c2r = args.st_rsplit ? mrow0 / args.st_rsplit : 0;
+        const CUtensorMap* cmap = &tmC;
+        if (args.rs_P) {
+          // whole tiles per block (block_rows % 128 == 0): pick the block's map
+          const int kr = u.m0 / args.rs_block_rows;
+          const int k = args.rs_block0 + kr;
+          c1 = mrow0 - kr * args.rs_block_rows;
+          cmap = &rsm.m[k];
+          if (k != args.rs_me && !(entered_mask & (1u << k))) {
+            if (lane == 0) ptx::wait_epoch(args.rs_entered[k], epoch);
+            __syncwarp();
+            entered_mask |= 1u << k;
+          }
+        }
         ptx::mbar_wait(&tfull_bar[acc], aph);
         ptx::tc_fence_after();
         const uint32_t row_taddr = tmem_base + acc * BN +
                                    (static_cast<uint32_t>(quarter * 32) << 16) + half * kColsPerWarp;
         const int ncol0 = u.n0 + half * kColsPerWarp;
         if (args.cw == 32)
-          epi_tile_tma<32, kColsPerWarp>(args, &tmC, &tmP, buf, lane, row_taddr, ncol0, row_off,
+          epi_tile_tma<32, kColsPerWarp>(args, cmap, &tmP, buf, lane, row_taddr, ncol0, row_off,
                                          row_ok, c1, c2r, c3, c4);
         else
           epi_tile_tma<(kColsPerWarp >= 64 ? 64 : 32), kColsPerWarp>(
-              args, &tmC, &tmP, buf, lane, row_taddr, ncol0, row_off, row_ok, c1, c2r, c3, c4);
+              args, cmap, &tmP, buf, lane, row_taddr, ncol0, row_off, row_ok, c1, c2r, c3, c4);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
@@ -518,7 +600,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           aph ^= 1;
         }
       }
-      if (lane == 0) ptx::bulk_wait_all();
+      if (lane == 0) {
+        ptx::bulk_wait_all();
+        if (args.rs_P) {
+          // this warp's peer-bound tile stores are complete: order them before the
+          // done flag raised below (system scope: the reader is another GPU)
+          ptx::fence_proxy_async_global();
+          __threadfence_system();
+        }
+      }
     } else
     for (int t = blockIdx.x; t < units; t += gridDim.x) {
       const Unit u = decode_unit(args, t, BN);
@@ -569,6 +659,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+  if (args.rs_P && threadIdx.x == 0) {
+    const uint32_t epoch = *args.rs_epoch;
+    __threadfence_system();
+    for (int k = 0; k < args.rs_P; ++k)
+      if (k != args.rs_me)
+        ptx::st_release_sys(args.rs_done[k] + args.rs_done_offset + blockIdx.x, epoch);
   }
 }
 
@@ -704,7 +801,8 @@ bool make_store_map(const View& v, long long rows, long long cols, int batch, in
 
 template <int BN, bool A_MN, bool B_MN>
 void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-               const CUtensorMap& mp, TcArgs& args, int num_sms, cudaStream_t stream) {
+               const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
+               cudaStream_t stream) {
   constexpr int kStageBytes = (kBM + BN) * kBK * 2;
   const int staging = args.tma_store ? kEpiWarps * 4096 : 0;
   int stages = (kSmemBudget - 1024 - 256 - staging) / kStageBytes;
@@ -718,17 +816,18 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     attr_set = true;
   }
   const int grid = std::min(args.num_tiles * args.ksplit, num_sms);
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mp, args);
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mp, args, rsm);
 }
 
 template <int BN>
 void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-               const CUtensorMap& mp, TcArgs& args, int num_sms, cudaStream_t stream) {
+               const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
+               cudaStream_t stream) {
   const bool am = args.a.mn_major, bm = args.b.mn_major;
-  if (!am && !bm) launch_tc<BN, false, false>(ma, mb, mc, mp, args, num_sms, stream);
-  else if (!am && bm) launch_tc<BN, false, true>(ma, mb, mc, mp, args, num_sms, stream);
-  else if (am && !bm) launch_tc<BN, true, false>(ma, mb, mc, mp, args, num_sms, stream);
-  else launch_tc<BN, true, true>(ma, mb, mc, mp, args, num_sms, stream);
+  if (!am && !bm) launch_tc<BN, false, false>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+  else if (!am && bm) launch_tc<BN, false, true>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+  else if (am && !bm) launch_tc<BN, true, false>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+  else launch_tc<BN, true, true>(ma, mb, mc, mp, args, rsm, num_sms, stream);
 }
 
 bool operand_ok(const View& v, long long rows, long long cols, int tile_rows) {
@@ -789,6 +888,32 @@ int tc_pick_bn(long long M, long long N, int batch, int num_sms) {
   return 128;
 }
 
+bool tc_gemm_rs_supported(const GemmProblem& p, int bn) {
+  const RsOut& r = p.rs;
+  if (r.P < 2 || r.P > kRsMax || p.batch != 1) return false;
+  if (r.block_rows <= 0 || r.block_rows % kBM || p.M % r.block_rows) return false;
+  if (r.block0 < 0 || r.block0 + p.M / r.block_rows > r.P) return false;
+  const int cw = p.epi.out.dtype == kF32 ? 32 : 64;
+  if (cw > bn / 2 || std::getenv("C3D_NO_TMA_STORE")) return false;
+  const Epilogue& e = p.epi;
+  if (e.bias || e.act != kActNone || e.pre_act || e.resid || e.accumulate || e.alpha != 1.f)
+    return false;
+  for (int k = r.block0; k < r.block0 + p.M / r.block_rows; ++k) {
+    View v;
+    v.base = r.dst[k];
+    v.dtype = e.out.dtype;
+    v.sr = p.N;
+    CUtensorMap m;
+    if (!make_store_map(v, r.block_rows, p.N, 1, cw, &m)) return false;
+  }
+  return true;
+}
+
+int tc_gemm_grid(const GemmProblem& p, int bn, int num_sms) {
+  const long long tiles = ((p.M + kBM - 1) / kBM) * ((p.N + bn - 1) / bn) * p.batch;
+  return static_cast<int>(std::min<long long>(tiles, num_sms));
+}
+
 bool tc_gemm_supported(const GemmProblem& p, int bn) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) return false;
   if (p.K % 8) return false;
@@ -809,7 +934,8 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.n_tiles = static_cast<int>((p.N + bn - 1) / bn);
   args.k_blocks = static_cast<int>((p.K + kBK - 1) / kBK);
   args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
-  args.ksplit = pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms);
+  args.ksplit = p.rs.P > 1 ? 1
+                            : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms);
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
   args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
   args.epi = p.epi;
@@ -859,14 +985,59 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     pv.dtype = p.epi.pre_dtype;
     tma = pv.dtype == sv.dtype && make_store_map(pv, p.M, p.N, p.batch, args.cw, &mp);
   }
+  RsMaps rsm;
+  std::memset(&rsm, 0, sizeof(rsm));
+  if (p.rs.P > 1) {
+    if (!tc_gemm_rs_supported(p, bn)) throw std::runtime_error("tc_gemm: fused reduce-scatter unsupported");
+    for (int k = 0; k < p.rs.P; ++k) {
+      args.rs_entered[k] = p.rs.entered[k];
+      args.rs_done[k] = p.rs.done[k];
+      if (k < p.rs.block0 || k >= p.rs.block0 + p.M / p.rs.block_rows) continue;
+      View v;
+      v.base = p.rs.dst[k];
+      v.dtype = p.epi.out.dtype;
+      v.sr = p.N;
+      make_store_map(v, p.rs.block_rows, p.N, 1, args.cw, &rsm.m[k]);
+    }
+    mc = rsm.m[p.rs.block0];
+    tma = true;
+    args.rs_P = p.rs.P;
+    args.rs_me = p.rs.me;
+    args.rs_block_rows = static_cast<int>(p.rs.block_rows);
+    args.rs_block0 = p.rs.block0;
+    args.rs_done_offset = p.rs.done_offset;
+    args.rs_epoch = p.rs.epoch;
+    sv = View();
+  }
+  if (p.ag.block_rows > 0) {
+    if (p.batch != 1 || p.ag.block_rows % kBM || p.M != 2 * p.ag.block_rows ||
+        args.ksplit != 1 || p.rs.P < 2 || (p.ag.block_rows * p.K * 2) % 16 ||
+        reinterpret_cast<uintptr_t>(p.ag.a_block[p.ag.own]) % 16)
+      throw std::runtime_error("tc_gemm: fused all-gather unsupported");
+    for (int k = 0; k < 2; ++k) {
+      View v = p.a;
+      v.base = const_cast<void*>(p.ag.a_block[k]);
+      TcOperand op;
+      rsm.ag[k] = make_operand_map(v, p.ag.block_rows, p.K, 1, kBM, &op);
+    }
+    args.ag_rows = static_cast<int>(p.ag.block_rows);
+    args.ag_own = p.ag.own;
+    args.m_rot = p.ag.own * static_cast<int>(p.ag.block_rows / kBM);
+    args.ag_src = static_cast<const char*>(p.ag.a_block[p.ag.own]);
+    args.ag_peer_dst = static_cast<char*>(p.ag.push_dst);
+    args.ag_own_dst = static_cast<char*>(p.ag.own_dst);
+    args.ag_bytes = p.ag.block_rows * p.K * 2;
+    args.ag_signal = p.ag.signal;
+    args.ag_wait = p.ag.wait;
+  }
   args.tma_store = tma ? 1 : 0;
   args.st_rsplit = static_cast<int>(sv.rsplit);
   args.st_csplit = static_cast<int>(sv.csplit);
   args.st_blo = sv.b_lo_n;
   switch (bn) {
-    case 64: launch_bn<64>(ma, mb, mc, mp, args, num_sms, stream); break;
-    case 128: launch_bn<128>(ma, mb, mc, mp, args, num_sms, stream); break;
-    case 256: launch_bn<256>(ma, mb, mc, mp, args, num_sms, stream); break;
+    case 64: launch_bn<64>(ma, mb, mc, mp, args, rsm, num_sms, stream); break;
+    case 128: launch_bn<128>(ma, mb, mc, mp, args, rsm, num_sms, stream); break;
+    case 256: launch_bn<256>(ma, mb, mc, mp, args, rsm, num_sms, stream); break;
     default: throw std::runtime_error("tc_gemm: unsupported BN");
   }
   if (args.ksplit > 1) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "cube.hpp"
@@ -15,6 +16,7 @@ namespace c3d {
 void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s);
 void prof_enable(bool on);
 void prof_read(double* ms, double* flops, long long* launches);
+void prof_read_comm(double* ms, double* bytes, long long* calls);
 
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
@@ -47,9 +49,26 @@ struct Vec {
 // has extent 1.
 struct Gathered {
   DevBuf buf;
+  std::unique_ptr<SymBuf> sym;  // gathered in place in the symmetric arena (fused path)
   const void* ptr = nullptr;
 };
 Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype, cudaStream_t s);
+
+// Local GEMM whose row blocks are reduce-scattered along `axis` inside its epilogue over
+// NVLink peer memory (fused.cu); `post` (out = this rank's contiguous result block) is
+// applied after the sum. Returns false (nothing launched) when the fused path does not
+// apply -- the decision is identical on every rank -- and the caller falls back.
+bool gemm_reduce_scatter(Cube& cube, int mode, int axis, int64_t M, int64_t N, int64_t K,
+                         const View& a, const View& b, const Epilogue& post, cudaStream_t s);
+// All-gather -> GEMM -> reduce-scatter with both transfers overlapped (lines of 2):
+// the shard (rows x K, K-major bf16) goes to the all-gather peer by copy engine while
+// the GEMM runs over the local rows; the peer's rows follow once they land; output row
+// blocks are reduce-scattered along rs_axis in the epilogue. `gathered` (optional)
+// receives the full gathered operand [2][rows][K].
+bool ag_gemm_rs(Cube& cube, int mode, int ag_axis, int rs_axis, const void* a_shard, int a_dtype,
+                int64_t rows, int64_t K, const View& b, int64_t N, const Epilogue& post,
+                Gathered* gathered, cudaStream_t s);
+
 
 // expand_diagonal (cube3d/ops3d.hpp:291-310): fp32 column block of length len/p_out
 // for an operand with triple d. Returns a stream-ordered fp32 buffer.

@@ -315,7 +315,6 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // a: (M/(Pw Pin)) x (N/Pout); b: (N/Pout) x (K/(Pin Pw))
-  Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
   Gathered bf;
   long long b_hi = b.rows * b.cols;
   if (bg && bg->ptr) {
@@ -325,14 +324,28 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
     bf = gather(cube, d.w, b.data, b.elems(), b.dtype, s);  // [Pw][N/Pout][K/(Pin Pw)]
   }
   const int64_t Mg = a.rows * Pin, Kg = a.cols, Ng = b.cols * Pw;
-  View av = kmajor(af.ptr, a.dtype, a.cols);
   View bv = mnmajor(bf.ptr, b.dtype, b.cols);
   if (Pw > 1) {
     bv.rsplit = b.cols;
     bv.s_hi = b_hi;
   }
-  if (keep_a) *keep_a = std::move(af);  // buffer (if any) outlives this call
   c = make_mat(cube, c.data, c.dtype, a.grows, b.gcols, kOutput, d.swapped());
+  if (Pin > 1 && Pout > 1) {
+    Epilogue f;
+    f.out = out_view(c.data, c.dtype, c.cols);
+    f.bias = le.bias;
+    f.act = le.act;
+    f.pre_act = le.pre_act;
+    f.pre_dtype = c.dtype;
+    f.resid = le.resid;
+    f.resid_dtype = c.dtype;
+    // gather, product and reduce-scatter as one overlapped operator over NVLink
+    if (ag_gemm_rs(cube, mode, d.in, d.out, a.data, a.dtype, a.rows, a.cols, bv, Ng, f, keep_a, s))
+      return;
+  }
+  Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+  View av = kmajor(af.ptr, a.dtype, a.cols);
+  if (keep_a) *keep_a = std::move(af);  // buffer (if any) outlives this call
   Epilogue e;
   if (Pout == 1) {
     e.out = out_view(c.data, c.dtype, c.cols);
@@ -345,21 +358,20 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
     local_gemm(cube, mode, Mg, Ng, Kg, av, bv, e, s);
     return;
   }
+  Epilogue f;
+  f.out = out_view(c.data, c.dtype, c.cols);
+  f.bias = le.bias;
+  f.act = le.act;
+  f.pre_act = le.pre_act;
+  f.pre_dtype = c.dtype;
+  f.resid = le.resid;
+  f.resid_dtype = c.dtype;
+  if (gemm_reduce_scatter(cube, mode, d.out, Mg, Ng, Kg, av, bv, f, s)) return;
   DevBuf partial(static_cast<size_t>(Mg * Ng) * dtype_size(c.dtype), s);
   e.out = out_view(partial.get(), c.dtype, Ng);
   local_gemm(cube, mode, Mg, Ng, Kg, av, bv, e, s);
   cube.reduce_scatter(d.out, partial.get(), c.data, c.elems(), c.dtype, s);
-  if (le.bias || le.act != kActNone || le.resid) {
-    Epilogue f;
-    f.out = out_view(c.data, c.dtype, c.cols);
-    f.bias = le.bias;
-    f.act = le.act;
-    f.pre_act = le.pre_act;
-    f.pre_dtype = c.dtype;
-    f.resid = le.resid;
-    f.resid_dtype = c.dtype;
-    k_apply_epilogue(c.data, c.dtype, c.rows, c.cols, f, s);
-  }
+  if (le.bias || le.act != kActNone || le.resid) k_apply_epilogue(c.data, c.dtype, c.rows, c.cols, f, s);
 }
 
 void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
@@ -368,7 +380,13 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // dC: (M/(Pw Pout)) x (K/Pin) with triple d.swapped(): gather along d.out
-  Gathered dcf = gather(cube, d.out, dc.data, dc.elems(), dc.dtype, s);  // (M/Pw) x (K/Pin)
+  Gathered dcf;
+  bool have_dcf = false;
+  const bool want_db = db && db->data;
+  auto need_dcf = [&] {
+    if (!have_dcf) dcf = gather(cube, d.out, dc.data, dc.elems(), dc.dtype, s);  // (M/Pw) x (K/Pin)
+    have_dcf = true;
+  };
   const int64_t Mrows = dc.rows * Pout, Kc = dc.cols;
   if (da && da->data) {
     Gathered bf;
@@ -381,14 +399,29 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
     }
     *da = make_mat(cube, da->data, da->dtype, a.grows, a.gcols, a.layout, a.dirs);
     // partial dA (M/Pw) x (N/Pout) = dc_full * b_full^T
-    View av = kmajor(dcf.ptr, dc.dtype, Kc);
     View bv = kmajor(bf.ptr, b.dtype, b.cols);
     if (Pw > 1) {
       bv.csplit = b.cols;
       bv.s_hi = b_hi;
     }
+    bool fused = false;
+    if (Pin > 1 && Pout > 1) {
+      Epilogue f;
+      f.out = out_view(da->data, da->dtype, da->cols);
+      if (da_gelu_aux) {
+        f.act = kActGeluGrad;
+        f.aux = da_gelu_aux;
+        f.aux_dtype = da->dtype;
+      }
+      fused = ag_gemm_rs(cube, mode, d.out, d.in, dc.data, dc.dtype, dc.rows, Kc, bv, b.rows, f,
+                         want_db ? &dcf : nullptr, s);
+      have_dcf = fused && want_db;
+    }
+    if (!fused) need_dcf();
+    View av = kmajor(dcf.ptr, dc.dtype, Kc);
     Epilogue e;
-    if (Pin == 1) {
+    if (fused) {
+    } else if (Pin == 1) {
       e.out = out_view(da->data, da->dtype, da->cols);
       if (da_gelu_aux) {
         e.act = kActGeluGrad;
@@ -397,21 +430,24 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
       }
       local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
     } else {
-      DevBuf partial(static_cast<size_t>(Mrows * b.rows) * dtype_size(da->dtype), s);
-      e.out = out_view(partial.get(), da->dtype, b.rows);
-      local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
-      cube.reduce_scatter(d.in, partial.get(), da->data, da->elems(), da->dtype, s);
+      Epilogue f;
+      f.out = out_view(da->data, da->dtype, da->cols);
       if (da_gelu_aux) {
-        Epilogue f;
-        f.out = out_view(da->data, da->dtype, da->cols);
         f.act = kActGeluGrad;
         f.aux = da_gelu_aux;
         f.aux_dtype = da->dtype;
-        k_apply_epilogue(da->data, da->dtype, da->rows, da->cols, f, s);
+      }
+      if (!gemm_reduce_scatter(cube, mode, d.in, Mrows, b.rows, Kc, av, bv, f, s)) {
+        DevBuf partial(static_cast<size_t>(Mrows * b.rows) * dtype_size(da->dtype), s);
+        e.out = out_view(partial.get(), da->dtype, b.rows);
+        local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
+        cube.reduce_scatter(d.in, partial.get(), da->data, da->elems(), da->dtype, s);
+        if (da_gelu_aux) k_apply_epilogue(da->data, da->dtype, da->rows, da->cols, f, s);
       }
     }
   }
-  if (db && db->data) {
+  if (want_db) {
+    need_dcf();
     Gathered af;
     if (ag) af.ptr = ag;
     else af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -94,6 +95,39 @@ __device__ __forceinline__ void bulk_wait_read() {
 // Waits until all committed bulk stores are complete.
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- cross-GPU flags
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Orders this thread's completed bulk-async (TMA) global writes before its later
+// generic-proxy operations (the release of a flag).
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Spins until *f reaches epoch e (wrap-safe). A peer that never arrives traps after
+// 30 s instead of hanging the GPU.
+__device__ inline void wait_epoch(const uint32_t* f, uint32_t e) {
+  if (static_cast<int32_t>(ld_acquire_sys(f) - e) >= 0) return;
+  const uint64_t t0 = globaltimer();
+  while (static_cast<int32_t>(ld_acquire_sys(f) - e) < 0) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > 30ull * 1000000000ull) {
+      printf("c3d: timeout waiting for a peer flag (epoch %u, have %u)\n", e, ld_acquire_sys(f));
+      __trap();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -410,6 +410,39 @@ class Cube:
     def reset_counters(self):
         call("c3d_counters_reset", self._h)
 
+    # --- Endpoint collectives along one axis (cube3d/transport.hpp:160-257)
+    def broadcast(self, axis: int, root_position: int, buf, stream=None):
+        """In place: every member of the axis line receives root_position's buf."""
+        call("c3d_broadcast", self._h, axis, root_position, C.c_void_p(buf.data_ptr()),
+             buf.numel(), c3d_dtype(buf), _stream(stream))
+        return buf
+
+    def all_gather(self, axis: int, shard, stream=None):
+        """-> (p * numel,) tensor: the members' shards in ascending position order."""
+        torch = _torch()
+        out = torch.empty(self.dims[axis] * shard.numel(), dtype=shard.dtype,
+                          device=shard.device)
+        call("c3d_all_gather", self._h, axis, C.c_void_p(shard.data_ptr()),
+             C.c_void_p(out.data_ptr()), shard.numel(), c3d_dtype(shard), _stream(stream))
+        return out
+
+    def reduce_scatter(self, axis: int, full, stream=None):
+        """full holds p equal blocks; -> this position's block of the elementwise sum."""
+        torch = _torch()
+        p = self.dims[axis]
+        if full.numel() % p:
+            raise C3DError(3, f"LengthMismatch: {full.numel()} elements not divisible by {p}")
+        out = torch.empty(full.numel() // p, dtype=full.dtype, device=full.device)
+        call("c3d_reduce_scatter", self._h, axis, C.c_void_p(full.data_ptr()),
+             C.c_void_p(out.data_ptr()), out.numel(), c3d_dtype(full), _stream(stream))
+        return out
+
+    def all_reduce(self, axis: int, buf, op: str = "sum", stream=None):
+        """In place sum (or max) over the axis line."""
+        call("c3d_all_reduce", self._h, axis, C.c_void_p(buf.data_ptr()), buf.numel(),
+             c3d_dtype(buf), 1 if op == "max" else 0, _stream(stream))
+        return buf
+
     def device_str(self):
         return f"cuda:{self.device}"
 
@@ -857,3 +890,10 @@ def prof_read():
     ms, fl, n = C.c_double(), C.c_double(), C.c_longlong()
     call("c3d_prof_read", C.byref(ms), C.byref(fl), C.byref(n))
     return ms.value, fl.value, n.value
+
+
+def prof_read_comm():
+    """-> (sum of collective times in ms, sum of payload bytes, calls)."""
+    ms, by, n = C.c_double(), C.c_double(), C.c_longlong()
+    call("c3d_prof_read_comm", C.byref(ms), C.byref(by), C.byref(n))
+    return ms.value, by.value, n.value

@@ -34,6 +34,52 @@ def gather_all(arr):
     return out
 
 
+def collective_checks(cube, dims):
+    """Endpoint collectives: the reference's transport KATs (tests/test_transport.cpp:
+    66-111) on every axis with extent 2, plus large payloads (multi-block, chunked
+    through the mailbox) against torch-computed expectations, f32 and bf16."""
+    dev = cube.device_str()
+    for axis in range(3):
+        if dims[axis] != 2:
+            continue
+        pos = cube.coords[axis]
+        f = torch.float32
+        base = 1.0 if pos == 0 else 3.0
+        ag = cube.all_gather(axis, torch.tensor([base, base + 1], dtype=f, device=dev))
+        mine = torch.tensor([1, 2, 3, 4] if pos == 0 else [10, 20, 30, 40], dtype=f, device=dev)
+        rs = cube.reduce_scatter(axis, mine)
+        ar = cube.all_reduce(axis, torch.tensor([1, 2] if pos == 0 else [3, 4], dtype=f,
+                                                device=dev))
+        mx = cube.all_reduce(axis, torch.tensor([1, 9] if pos == 0 else [3, 4], dtype=f,
+                                                device=dev), op="max")
+        bc = torch.tensor([1, 2, 3, 4] if pos == 1 else [0, 0, 0, 0], dtype=f, device=dev)
+        cube.broadcast(axis, 1, bc)
+        torch.cuda.synchronize()
+        ok = (ag.tolist() == [1, 2, 3, 4] and rs.tolist() == ([11, 22] if pos == 0 else [33, 44])
+              and ar.tolist() == [4, 6] and mx.tolist() == [3, 9] and bc.tolist() == [1, 2, 3, 4])
+        oks = gather_all(ok)
+        report(f"collectives-kat-axis{axis}", all(oks))
+        # large integer-valued payloads (exact in bf16 and f32), odd sizes hit the
+        # scalar path; 40M f32 elements exceed one mailbox slot and are chunked
+        for dt in (torch.float32, torch.bfloat16):
+            for n in (1000003, 4 << 20, 40 << 20 if dt == torch.float32 else 8 << 20):
+                g = torch.Generator(device="cpu").manual_seed(7 + n)
+                full = torch.randint(0, 8, (2, 2 * n if n < (40 << 20) else n), generator=g)
+                full = full.to(dt)
+                m = full.shape[1]
+                mine = full[pos].to(dev)
+                got_ag = cube.all_gather(axis, mine)
+                got_rs = cube.reduce_scatter(axis, mine)
+                got_ar = cube.all_reduce(axis, mine.clone())
+                torch.cuda.synchronize()
+                exp_sum = (full[0].float() + full[1].float()).to(dt)
+                ok = (torch.equal(got_ag.cpu(), full.reshape(-1))
+                      and torch.equal(got_rs.cpu(), exp_sum[pos * (m // 2):(pos + 1) * (m // 2)])
+                      and torch.equal(got_ar.cpu(), exp_sum))
+                oks = gather_all(bool(ok))
+                report(f"collectives-axis{axis}-{str(dt)[6:]}-n{m}", all(oks))
+
+
 def matmul_checks(cube, dims):
     q = dims[0] * dims[1] * dims[2]
     n = 4 * q * q if q > 1 else 32
@@ -132,6 +178,7 @@ def main():
     torch.cuda.set_device(local)
     dims = c3.grid_for(world) if len(sys.argv) < 2 else tuple(int(v) for v in sys.argv[1].split("x"))
     cube = cdist.make_cube(dims)
+    collective_checks(cube, dims)
     if os.environ.get("MP_SKIP_MATMUL") is None:
         matmul_checks(cube, dims)
     if dims[1] == dims[2]:
