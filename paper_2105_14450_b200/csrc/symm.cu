@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -91,7 +92,7 @@ struct Lane {
 };
 
 template <int DT, bool VEC>
-__global__ void __launch_bounds__(512) symm_coll_kernel(const SymmArgs a) {
+__global__ void __launch_bounds__(1024) symm_coll_kernel(const SymmArgs a) {
   using L = Lane<DT, VEC>;
   constexpr int B = L::kBytes;
   const int b = blockIdx.x;
@@ -201,7 +202,11 @@ __global__ void __launch_bounds__(512) symm_coll_kernel(const SymmArgs a) {
 
 template <int DT, bool VEC>
 void launch(const SymmArgs& a, cudaStream_t s) {
-  symm_coll_kernel<DT, VEC><<<a.G, 512, 0, s>>>(a);
+  static const int threads = [] {
+    const char* e = std::getenv("C3D_SYMM_THREADS");
+    return e ? std::atoi(e) : 512;
+  }();
+  symm_coll_kernel<DT, VEC><<<a.G, threads, 0, s>>>(a);
 }
 
 }  // namespace
@@ -349,10 +354,18 @@ void SymmHeap::collective(CollOp op, const std::vector<int>& line, int pos, cons
     const size_t n = std::min(cap, count - c0);
     a.c0 = static_cast<long long>(c0);
     a.n = static_cast<long long>(n);
-    // one block per 32 KB of payload, at most two per SM (all co-resident)
-    const size_t blocks = (n * es + 32767) / 32768;
-    a.G = static_cast<int>(
-        std::max<size_t>(1, std::min<size_t>(blocks, std::min(2 * num_sms, kSymmMaxBlocks))));
+    // one block per `chunk` bytes of payload, at most `per_sm` per SM (all co-resident)
+    static const size_t chunk = [] {
+      const char* e = std::getenv("C3D_SYMM_CHUNK_KB");
+      return static_cast<size_t>(e ? std::atoi(e) : 32) << 10;
+    }();
+    static const int per_sm = [] {
+      const char* e = std::getenv("C3D_SYMM_PER_SM");
+      return e ? std::atoi(e) : 2;
+    }();
+    const size_t blocks = (n * es + chunk - 1) / chunk;
+    a.G = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(blocks, std::min(per_sm * num_sms, kSymmMaxBlocks))));
     if (dtype == kF32) {
       if (vec_ok) launch<kF32, true>(a, s); else launch<kF32, false>(a, s);
     } else {

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--axis", type=int, default=0)
     ap.add_argument("--iters", type=int, default=50)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--graph", action="store_true", help="time a captured CUDA graph of the calls")
+    ap.add_argument("--sizes", default="0.03,0.5,2,8,16,32,64")
     args = ap.parse_args()
     rank, world, local = cdist.init_process_group("nccl")
     torch.cuda.set_device(local)
@@ -39,7 +41,7 @@ def main():
             w @ w
         torch.cuda.synchronize()
     tag = "nccl" if os.environ.get("C3D_NCCL_COLL") else "symm"
-    for mb in (0.03, 0.5, 2, 8, 16, 32, 64):
+    for mb in [float(v) for v in args.sizes.split(",")]:
         n = int(mb * 1e6 / es) // 64 * 64
         full = torch.ones(n, dtype=dt, device="cuda")
         shard = torch.ones(n // p, dtype=dt, device="cuda")
@@ -50,11 +52,23 @@ def main():
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
+            g = None
+            if args.graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    for _ in range(args.iters):
+                        fn()
+                torch.cuda.synchronize()
+                g.replay()
+                torch.cuda.synchronize()
             cdist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(args.iters):
-                fn()
+            if g is not None:
+                g.replay()
+            else:
+                for _ in range(args.iters):
+                    fn()
             e1.record()
             torch.cuda.synchronize()
             us = cdist.max_over_ranks(e0.elapsed_time(e1) / args.iters * 1e3)
