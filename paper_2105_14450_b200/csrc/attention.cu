@@ -1,0 +1,273 @@
+// Fused attention core for one rank whose slices hold the whole key range (the seq
+// axis of the cube has extent 1): per (slice, 128-query tile) CTA
+//
+//   S = Q K^T                 tcgen05, Q/K staged by TMA, S (128 x keys fp32) in TMEM
+//   P = softmax(scale * S)    epilogue warps, one query row per thread, fp32
+//   P -> shared (bf16, UMMA K-major 128B-swizzled) -> global probs (TMA store, saved
+//        for the backward exactly as the unfused path saves them)
+//   O = P V                   tcgen05 with P from shared memory, V staged MN-major
+//   O -> ctx (bf16)
+//
+// It replaces, for that case, the scores GEMM with its fp32 score buffer, the softmax
+// kernel and the P V GEMM of attention_fwd (cube3d/attention.hpp:95-127): the scores
+// never leave the SM. Limits: head dim 64, keys a multiple of 256 up to 512 (TMEM
+// holds one full score row block: 512 fp32 columns), queries a multiple of 128.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "common.hpp"
+#include "gemm.hpp"
+#include "gemm_tc.hpp"
+#include "kernels.hpp"
+#include "ptx.cuh"
+
+namespace c3d {
+
+namespace {
+
+constexpr int kQ = 128;   // queries per CTA (UMMA M)
+constexpr int kDh = 64;   // head dim (one 128-B K block)
+constexpr int kThreadsAttn = 192;  // warp 0 TMA, warp 1 MMA, warps 2..5 softmax rows
+
+struct AttnArgs {
+  int S, keys, H;
+  float scale_log2;  // scale * log2(e)
+  __nv_bfloat16* ctx;
+  long long ctx_sr, ctx_sb_lo, ctx_sb_hi;  // element strides of the context view
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int KEYS>
+__global__ void __launch_bounds__(kThreadsAttn, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmP,
+                    const AttnArgs args) {
+  constexpr int kQBytes = kQ * kDh * 2;              // 16 KB
+  constexpr int kKBytes = KEYS * kDh * 2;            // keys x 128 B
+  constexpr int kPBytes = KEYS / 64 * kQ * 128;      // 64-key chunks of [128 rows][128 B]
+  constexpr int kVOff = (kQBytes + kKBytes > kPBytes ? kQBytes + kKBytes : kPBytes);
+  constexpr int kVBytes = KEYS * kDh * 2;
+  constexpr uint32_t kIdescS = ptx::idesc_bf16_f32(kQ, 256, false, false);
+  constexpr uint32_t kIdescO = ptx::idesc_bf16_f32(kQ, kDh, false, true);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + kQBytes;
+  uint8_t* sP = smem;  // overwrites Q and K once S is in TMEM
+  uint8_t* sV = smem + kVOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kVOff + kVBytes);
+  uint64_t* bar_qk = bars;
+  uint64_t* bar_v = bars + 1;
+  uint64_t* bar_s = bars + 2;
+  uint64_t* bar_p = bars + 3;
+  uint64_t* bar_o = bars + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int q0 = blockIdx.x * kQ;
+  const int b = blockIdx.y;
+  const int c3 = b % args.H, c4 = b / args.H;
+
+  if (warp == 0 && lane == 0) {
+    ptx::mbar_init(bar_qk, 1);
+    ptx::mbar_init(bar_v, 1);
+    ptx::mbar_init(bar_s, 1);
+    ptx::mbar_init(bar_p, 128);
+    ptx::mbar_init(bar_o, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(bar_qk, kQBytes + kKBytes);
+      ptx::tma_load_5d(sQ, &tmQ, bar_qk, 0, q0, 0, c3, c4);
+#pragma unroll
+      for (int h = 0; h < KEYS / 256; ++h)
+        ptx::tma_load_5d(sK + h * 256 * 128, &tmK, bar_qk, 0, h * 256, 0, c3, c4);
+      ptx::mbar_arrive_expect_tx(bar_v, kVBytes);
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+        ptx::tma_load_5d(sV + kb * 8192, &tmV, bar_v, 0, kb * 64, 0, c3, c4);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(bar_qk, 0);
+      ptx::tc_fence_after();
+      const uint32_t qa = ptx::smem_u32(sQ), ka = ptx::smem_u32(sK);
+#pragma unroll
+      for (int h = 0; h < KEYS / 256; ++h)
+#pragma unroll
+        for (int k = 0; k < kDh / 16; ++k)
+          ptx::umma_bf16(tmem + h * 256, ptx::smem_desc_sw128(qa + 32 * k, 16, 1024),
+                         ptx::smem_desc_sw128(ka + h * 256 * 128 + 32 * k, 16, 1024), kIdescS,
+                         k > 0 ? 1u : 0u);
+      ptx::umma_commit(bar_s);
+      // O = P V once the softmax warps have written P and released the S columns
+      ptx::mbar_wait(bar_p, 0);
+      ptx::mbar_wait(bar_v, 0);
+      ptx::tc_fence_after();
+      const uint32_t pa = ptx::smem_u32(sP), va = ptx::smem_u32(sV);
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          ptx::umma_bf16(tmem, ptx::smem_desc_sw128(pa + kb * 16384 + 32 * k, 16, 1024),
+                         ptx::smem_desc_sw128(va + kb * 8192 + 2048 * k, 8192, 1024), kIdescO,
+                         (kb > 0 || k > 0) ? 1u : 0u);
+      ptx::umma_commit(bar_o);
+    }
+  } else {
+    // ---------------- softmax rows: warp w owns TMEM lanes 32*(w % 4) .. +32
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    ptx::mbar_wait(bar_s, 0);
+    ptx::tc_fence_after();
+    float m = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < KEYS / 32; ++c) {
+      float v[32];
+      ptx::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) m = fmaxf(m, v[j]);
+    }
+    const float ms = m * args.scale_log2;
+    float sum = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < KEYS / 32; ++c) {
+      float v[32];
+      ptx::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(v[j], args.scale_log2, -ms));
+    }
+    const float inv = 1.f / sum;
+#pragma unroll 1
+    for (int c = 0; c < KEYS / 32; ++c) {
+      float v[32];
+      ptx::tmem_ld32(trow + c * 32, v);
+      uint8_t* chunk_row = sP + (c >> 1) * 16384 + row * 128;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 pk;
+        pk.x = pack_bf16(exp2f(fmaf(v[8 * j + 0], args.scale_log2, -ms)) * inv,
+                         exp2f(fmaf(v[8 * j + 1], args.scale_log2, -ms)) * inv);
+        pk.y = pack_bf16(exp2f(fmaf(v[8 * j + 2], args.scale_log2, -ms)) * inv,
+                         exp2f(fmaf(v[8 * j + 3], args.scale_log2, -ms)) * inv);
+        pk.z = pack_bf16(exp2f(fmaf(v[8 * j + 4], args.scale_log2, -ms)) * inv,
+                         exp2f(fmaf(v[8 * j + 5], args.scale_log2, -ms)) * inv);
+        pk.w = pack_bf16(exp2f(fmaf(v[8 * j + 6], args.scale_log2, -ms)) * inv,
+                         exp2f(fmaf(v[8 * j + 7], args.scale_log2, -ms)) * inv);
+        const int chunk = (c & 1) * 4 + j;
+        *reinterpret_cast<uint4*>(chunk_row + ((chunk ^ (row & 7)) << 4)) = pk;
+      }
+    }
+    // P visible to the tensor core (async proxy); S columns free for O
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(bar_p);
+    // probabilities to global (saved for the backward): one TMA store per 64-key chunk
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 2 && lane == 0) {
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+        ptx::tma_store_5d(&tmP, sP + kb * 16384, kb * 64, q0, 0, c3, c4);
+      ptx::bulk_commit();
+    }
+    // context row: O (fp32 in TMEM columns 0..63) -> bf16
+    ptx::mbar_wait(bar_o, 0);
+    ptx::tc_fence_after();
+    float o[64];
+    ptx::tmem_ld32(trow, *reinterpret_cast<float(*)[32]>(o));
+    ptx::tmem_ld32(trow + 32, *reinterpret_cast<float(*)[32]>(o + 32));
+    __nv_bfloat16* dst = args.ctx + c3 * args.ctx_sb_lo + c4 * args.ctx_sb_hi +
+                         static_cast<long long>(q0 + row) * args.ctx_sr;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 pk;
+      pk.x = pack_bf16(o[8 * j + 0], o[8 * j + 1]);
+      pk.y = pack_bf16(o[8 * j + 2], o[8 * j + 3]);
+      pk.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
+      pk.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
+      reinterpret_cast<uint4*>(dst)[j] = pk;
+    }
+    if (warp == 2 && lane == 0) ptx::bulk_wait_all();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int KEYS>
+void launch_attn(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
+                 const CUtensorMap& p, const AttnArgs& a, int nslices, cudaStream_t s) {
+  constexpr int kQBytes = kQ * kDh * 2, kKBytes = KEYS * kDh * 2;
+  constexpr int kPBytes = KEYS / 64 * kQ * 128;
+  constexpr int kVOff = (kQBytes + kKBytes > kPBytes ? kQBytes + kKBytes : kPBytes);
+  constexpr int smem = 1024 + kVOff + KEYS * kDh * 2 + 64;
+  auto kern = attn_fwd_kernel<KEYS>;
+  static bool attr = false;
+  if (!attr) {
+    C3D_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  kern<<<dim3(a.S / kQ, nslices), kThreadsAttn, smem, s>>>(q, k, v, p, a);
+}
+
+}  // namespace
+
+bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
+                    int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
+                    cudaStream_t s) {
+  if (std::getenv("C3D_NO_FUSED_ATTN")) return false;
+  if (dh != kDh || S % kQ || (keys != 256 && keys != 512) || H <= 0) return false;
+  for (const View* w : {&q, &k, &v, &probs, &ctx})
+    if (w->dtype != kBF16 || reinterpret_cast<uintptr_t>(w->base) % 16) return false;
+  if (q.rsplit || q.csplit || k.rsplit || k.csplit || v.rsplit || v.csplit || probs.rsplit ||
+      probs.csplit || ctx.rsplit || ctx.csplit)
+    return false;
+  if (ctx.sc != 1 || (ctx.sr * 2) % 16 || (ctx.sb_lo * 2) % 16 || (ctx.sb_hi * 2) % 16) return false;
+  if (ctx.b_lo_n != H || q.b_lo_n != H || k.b_lo_n != H || v.b_lo_n != H || probs.b_lo_n != H)
+    return false;
+  int mn = 0;
+  const CUtensorMap mq = tc_operand_map(q, S, dh, nslices, kQ, &mn);
+  if (mn) return false;
+  const CUtensorMap mk = tc_operand_map(k, keys, dh, nslices, 256, &mn);
+  if (mn) return false;
+  const CUtensorMap mv = tc_operand_map(v, dh, keys, nslices, 64, &mn);
+  if (!mn) return false;
+  CUtensorMap mp;
+  if (!tc_store_map(probs, S, keys, nslices, 64, kQ, &mp)) return false;
+  AttnArgs a{};
+  a.S = static_cast<int>(S);
+  a.keys = static_cast<int>(keys);
+  a.H = static_cast<int>(H);
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.ctx = static_cast<__nv_bfloat16*>(ctx.base);
+  a.ctx_sr = ctx.sr;
+  a.ctx_sb_lo = ctx.sb_lo;
+  a.ctx_sb_hi = ctx.sb_hi;
+  if (keys == 512) launch_attn<512>(mq, mk, mv, mp, a, nslices, s);
+  else launch_attn<256>(mq, mk, mv, mp, a, nslices, s);
+  check_launch("attn_fwd_fused");
+  return true;
+}
+
+}  // namespace c3d

@@ -136,15 +136,22 @@ __global__ void __launch_bounds__(256) rs_finish_kernel(const FinishArgs a) {
         acc[0] += b0.x; acc[1] += b0.y; acc[2] += b0.z; acc[3] += b0.w;
         acc[4] += b1.x; acc[5] += b1.y; acc[6] += b1.z; acc[7] += b1.w;
       }
-      if (e.pre_act) store8<DT>(static_cast<char*>(e.pre_act) + off * es, acc);
+      if (e.act == kActGeluSave) {
+        float gd[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) gelu_both(acc[j], acc[j], gd[j]);
+        if (e.pre_act) store8<DT>(static_cast<char*>(e.pre_act) + off * es, gd);
+      } else if (e.pre_act) {
+        store8<DT>(static_cast<char*>(e.pre_act) + off * es, acc);
+      }
       if (e.act == kActGelu) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = gelu_f(acc[j]);
-      } else if (e.act == kActGeluGrad) {
+      } else if (e.act == kActGeluGrad || e.act == kActMulAux) {
         float g[8];
         load8<DT>(static_cast<const char*>(e.aux) + off * es, g, false);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] *= gelu_grad_f(g[j]);
+        for (int j = 0; j < 8; ++j) acc[j] *= e.act == kActMulAux ? g[j] : gelu_grad_f(g[j]);
       }
       if (e.resid) {
         float r[8];
@@ -190,7 +197,7 @@ void launch_finish(Cube& cube, SymmHeap* h, int axis, int grid, int done_offset,
   fa.e = post;
   auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
   bool vec = cols % 8 == 0 && al(post.out.base) && post.out.sr == cols && post.alpha == 1.f &&
-             !post.accumulate && (!post.bias || al(post.bias));
+             !post.accumulate && (!post.bias || al(post.bias)) && post.act != kActSoftmaxBwd;
   for (const void* q : {static_cast<const void*>(post.pre_act), post.aux, post.resid})
     vec = vec && (!q || al(q));
   vec = vec && (!post.pre_act || post.pre_dtype == dtype) &&
@@ -306,72 +313,6 @@ bool gemm_reduce_scatter(Cube& cube, int mode, int axis, int64_t M, int64_t N, i
   }
   cube.account(C3D_REDUCE_SCATTER, static_cast<uint64_t>(P - 1) * slot_elems,
                static_cast<uint64_t>(P - 1) * slot_elems);
-  return true;
-}
-
-bool ag_gemm_rs(Cube& cube, int mode, int ag_axis, int rs_axis, const void* a_shard, int a_dtype,
-                int64_t rows, int64_t K, const View& b, int64_t N, const Epilogue& post,
-                Gathered* gathered, cudaStream_t s) {
-  SymmHeap* h = cube.symm();
-  if (!h || mode == C3D_MODE_F32 || a_dtype != kBF16 || b.dtype != kBF16) return false;
-  if (cube.extent(ag_axis) != 2 || cube.extent(rs_axis) != 2 || ag_axis == rs_axis) return false;
-  // opt-in: on this pool the in-kernel push (one warp per CTA) does not yet beat a
-  // separate all-gather followed by the fused GEMM + reduce-scatter
-  if (rows % 128 || !std::getenv("C3D_FUSED_AG") || std::getenv("C3D_NO_FUSED_RS")) return false;
-  const int i = cube.coord(ag_axis);
-  const int peer_ag = cube.line(ag_axis)[1 - i];
-  const int dtype = post.out.dtype;
-  const long long es = dtype == kF32 ? 4 : 2;
-  const long long shard_bytes = rows * K * 2;
-  const long long M = 2 * rows;
-  const long long block_rows = rows;  // reduce-scatter blocks (lines of 2)
-  const long long slot_elems = block_rows * N;
-  auto g = std::make_unique<SymBuf>(h, static_cast<size_t>(2 * shard_bytes));
-  SymBuf recv(h, static_cast<size_t>(2 * slot_elems * es));
-  if (!g->ok() || !recv.ok()) return false;
-
-  GemmProblem p;
-  p.M = M;
-  p.N = N;
-  p.K = K;
-  p.a = kview(g->local(), kBF16, K);
-  p.b = b;
-  p.epi.out = kview(recv.local(), dtype, N);
-  fill_rs(cube, h, rs_axis, recv, block_rows, slot_elems * es, 0, 0, &p.rs);
-  p.ag.block_rows = rows;
-  p.ag.own = i;
-  p.ag.a_block[i] = a_shard;
-  p.ag.a_block[1 - i] = g->local() + (1 - i) * shard_bytes;
-  p.ag.push_dst = g->at(peer_ag) + i * shard_bytes;
-  p.ag.own_dst = gathered ? g->local() + i * shard_bytes : nullptr;
-  p.ag.signal = h->op_ag(peer_ag) + static_cast<size_t>(cube.rank()) * kSymmMaxBlocks;
-  p.ag.wait = h->op_ag(cube.rank()) + static_cast<size_t>(peer_ag) * kSymmMaxBlocks;
-  const int bn = tc_pick_bn(M, N, 1, cube.num_sms());
-  if (!tc_gemm_supported(p, bn) || !tc_gemm_rs_supported(p, bn)) return false;
-  const int grid = tc_gemm_grid(p, bn, cube.num_sms());
-  if (grid > kSymmMaxBlocks) return false;
-
-  const int peer_rs = cube.line(rs_axis)[1 - cube.coord(rs_axis)];
-  {
-    Span sp(s, 5, 0);
-    launch_enter(cube, h, {peer_ag, peer_rs}, true, s);
-  }
-  {
-    Span sp(s, 7, static_cast<double>(2 * slot_elems * es));
-    run_gemm(p, C3D_MODE_TC, cube.num_sms(), s);
-  }
-  cube.add_madds(static_cast<uint64_t>(M) * N * K);
-  {
-    Span sp(s, 8, static_cast<double>(2 * slot_elems * es));
-    launch_finish(cube, h, rs_axis, grid, 0, recv.local(), slot_elems, block_rows, N, post, s);
-  }
-  cube.account(C3D_ALL_GATHER, static_cast<uint64_t>(rows * K), static_cast<uint64_t>(rows * K));
-  cube.account(C3D_REDUCE_SCATTER, static_cast<uint64_t>(slot_elems),
-               static_cast<uint64_t>(slot_elems));
-  if (gathered) {
-    gathered->ptr = g->local();
-    gathered->sym = std::move(g);
-  }
   return true;
 }
 

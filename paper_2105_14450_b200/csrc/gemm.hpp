@@ -44,7 +44,18 @@ __host__ __device__ inline long long view_offset(const View& v, long long b, lon
   return off;
 }
 
-enum ActKind : int { kActNone = 0, kActGelu = 1, kActGeluGrad = 2 };
+// kActGeluSave: gelu, and the pre-activation output receives gelu'(x) instead of x (the
+//   backward then only multiplies: kActMulAux).
+// kActSoftmaxBwd: v = aux * (v - alpha * rowvec[off / rv_div]) (softmax backward with the
+//   row dot product precomputed; alpha already applied to v).
+enum ActKind : int {
+  kActNone = 0,
+  kActGelu = 1,
+  kActGeluGrad = 2,
+  kActGeluSave = 3,
+  kActMulAux = 4,
+  kActSoftmaxBwd = 5
+};
 
 // Fused epilogue, applied per output element in this order:
 //   v = alpha*acc; v += bias[n]; pre = v (stored if pre_act);
@@ -64,6 +75,8 @@ struct Epilogue {
   const void* resid = nullptr;
   int resid_dtype = kBF16;
   int accumulate = 0;
+  const float* rowvec = nullptr;  // kActSoftmaxBwd
+  long long rv_div = 1;
 };
 
 // Reduce-scatter fused into the tcgen05 GEMM epilogue: C's rows form P blocks of
@@ -84,30 +97,12 @@ struct RsOut {
   const uint32_t* epoch = nullptr;
 };
 
-// All-gather fused into the GEMM (lines of 2, with a fused reduce-scatter whose epoch it
-// shares): A's rows form 2 blocks of block_rows, block k read from a_block[k]
-// ([block_rows][K] K-major bf16; a_block[own] is this rank's shard). A dedicated warp
-// per CTA pushes 1/grid of the shard to push_dst (this rank's slot in the peer's
-// gathered buffer) and own_dst (optional local copy), then raises signal[cta]. Own-block
-// tiles are scheduled first; before loading the other block the TMA producer waits
-// for every peer CTA's flag in wait[].
-struct AgIn {
-  long long block_rows = 0;  // 0: plain operand A
-  int own = 0;
-  const void* a_block[2] = {};
-  void* push_dst = nullptr;
-  void* own_dst = nullptr;
-  uint32_t* signal = nullptr;
-  const uint32_t* wait = nullptr;
-};
-
 struct GemmProblem {
   long long M = 0, N = 0, K = 0;
   int batch = 1;
   View a, b;  // a: [batch][M][K], b: [batch][N][K]
   Epilogue epi;
   RsOut rs;
-  AgIn ag;
 };
 
 }  // namespace c3d

@@ -20,6 +20,8 @@ struct ProfRec {
   double flops;  // GEMM flops, or collective payload bytes
   int kind;      // 0 = tcgen05 GEMM, 1 = collective
   int tag;       // collective kind (C3D_BROADCAST ...)
+  long long M, N, K;
+  int batch, bn, amn, bmn, outdt;
 };
 
 struct Profiler {
@@ -42,6 +44,17 @@ struct Profiler {
 Profiler& prof() {
   static Profiler p;
   return p;
+}
+
+// Inside stream capture an event must be recorded as an external event node to stay
+// a real (timed) event in the graph.
+void record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  C3D_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st == cudaStreamCaptureStatusActive)
+    C3D_CUDA(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+  else
+    C3D_CUDA(cudaEventRecord(e, s));
 }
 
 }  // namespace
@@ -68,12 +81,21 @@ void read_kind(int kind, double* ms, double* amount, long long* count) {
       rest.push_back(r);
       continue;
     }
-    C3D_CUDA(cudaEventSynchronize(r.stop));
     float x = 0;
-    C3D_CUDA(cudaEventElapsedTime(&x, r.start, r.stop));
+    if (cudaEventSynchronize(r.stop) != cudaSuccess ||
+        cudaEventElapsedTime(&x, r.start, r.stop) != cudaSuccess) {
+      cudaGetLastError();
+      continue;  // unreadable (e.g. never replayed): dropped
+    }
     if (dump && kind == 1)
       std::fprintf(stderr, "[c3d prof] coll kind=%d bytes=%.0f us=%.1f GB/s=%.1f\n", r.tag, r.flops,
                    1e3 * x, x > 0 ? r.flops / (x * 1e6) : 0.0);
+    if (dump && kind == 0)
+      std::fprintf(stderr,
+                   "[c3d prof] gemm M=%lld N=%lld K=%lld batch=%d bn=%d a_mn=%d b_mn=%d out=%s "
+                   "us=%.1f TF/s=%.1f\n",
+                   r.M, r.N, r.K, r.batch, r.bn, r.amn, r.bmn, r.outdt == kF32 ? "f32" : "bf16",
+                   1e3 * x, x > 0 ? r.flops / (x * 1e9) : 0.0);
     if (kind == 1 && r.tag >= 5) continue;  // fused-operator spans: dumped, not summed
     t += x;
     f += r.flops;
@@ -103,7 +125,7 @@ void prof_begin(cudaStream_t s, void** token) {
   Profiler& pr = prof();
   std::lock_guard<std::mutex> g(pr.mu);
   cudaEvent_t e = pr.take();
-  C3D_CUDA(cudaEventRecord(e, s));
+  record(e, s);
   *token = e;
 }
 
@@ -116,7 +138,7 @@ void prof_end(cudaStream_t s, void* token, int tag, double bytes) {
   rec.flops = bytes;
   rec.kind = 1;
   rec.tag = tag;
-  C3D_CUDA(cudaEventRecord(rec.stop, s));
+  record(rec.stop, s);
   pr.recs.push_back(rec);
 }
 
@@ -135,13 +157,21 @@ void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s) {
         rec.stop = pr.take();
         rec.flops = 2.0 * p.M * p.N * p.K * p.batch;
         rec.kind = 0;
-        C3D_CUDA(cudaEventRecord(rec.start, s));
+        rec.M = p.M;
+        rec.N = p.N;
+        rec.K = p.K;
+        rec.batch = p.batch;
+        rec.bn = bn;
+        rec.amn = p.a.sr == 1 && p.a.sc != 1;
+        rec.bmn = p.b.sr == 1 && p.b.sc != 1;
+        rec.outdt = p.epi.out.dtype;
+        record(rec.start, s);
       }
       tc_gemm_launch(p, bn, num_sms, s);
       check_launch("tc_gemm");
       if (on) {
         std::lock_guard<std::mutex> g(pr.mu);
-        C3D_CUDA(cudaEventRecord(rec.stop, s));
+        record(rec.stop, s);
         pr.recs.push_back(rec);
       }
       return;

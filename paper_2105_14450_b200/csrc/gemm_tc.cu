@@ -40,8 +40,7 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kEpiWarps = 8;
-constexpr int kCommWarp = 2 + kEpiWarps;  // pushes the all-gather shard (fused mode)
-constexpr int kThreads = 64 + 32 * kEpiWarps + 32;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kSmemBudget = 227 * 1024;
 
 struct TcOperand {
@@ -64,6 +63,10 @@ struct TcArgs {
   int cw;                    // columns per store chunk (32 fp32, 64 bf16)
   int st_rsplit, st_csplit;  // split of the stored view (rows / cols)
   int st_blo;                // batch-lo extent of the stored view
+  int x_tma;                 // 1: aux tile chunks arrive by TMA (tmP) into a second
+                             //    per-warp buffer (same view geometry as the output)
+  int pre_tma;               // 1: the pre-activation output is staged in that second
+                             //    buffer and TMA-stored through tmP
   TcOperand a, b;
   Epilogue epi;
   // fused reduce-scatter (rs_P > 1): block k of the rows goes through rsm.m[k]
@@ -71,20 +74,10 @@ struct TcArgs {
   const uint32_t* rs_entered[kRsMax];
   uint32_t* rs_done[kRsMax];
   const uint32_t* rs_epoch;
-  // fused all-gather (ag_rows > 0): A row block k through agm.m[k]; tiles rotated so the
-  // own block comes first; the other block waits for *ag_ready == 1
-  int ag_rows, ag_own, m_rot;
-  const char* ag_src;       // this rank's shard
-  char* ag_peer_dst;        // its slot in the peer's gathered buffer (NVLink mapping)
-  char* ag_own_dst;         // its slot in the local gathered buffer (null: not kept)
-  long long ag_bytes;
-  uint32_t* ag_signal;      // peer's arrival flags for this rank, [cta]
-  const uint32_t* ag_wait;  // this rank's arrival flags for the peer, [cta]
 };
 
 struct RsMaps {
   CUtensorMap m[kRsMax];
-  CUtensorMap ag[2];
 };
 
 // Writes one 32-value row segment (CW = 32 fp32 or 64 bf16 values = 128 B) into row
@@ -111,6 +104,27 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v
       pk.w = *reinterpret_cast<uint32_t*>(&h3);
       *reinterpret_cast<uint4*>(dst) = pk;
     }
+  }
+}
+
+// Writes one 16-B chunk j (8 bf16 or 4 fp32 values) of row `lane` of the swizzled
+// staging tile.
+template <int CW>
+__device__ __forceinline__ void stage_chunk(uint8_t* buf, int lane, int j, const float* v) {
+  uint8_t* dst = buf + lane * 128 + ((j ^ (lane & 7)) << 4);
+  if (CW == 32) {
+    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+    uint4 pk;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 h1 = __floats2bfloat162_rn(v[2], v[3]);
+    __nv_bfloat162 h2 = __floats2bfloat162_rn(v[4], v[5]);
+    __nv_bfloat162 h3 = __floats2bfloat162_rn(v[6], v[7]);
+    pk.x = *reinterpret_cast<uint32_t*>(&h0);
+    pk.y = *reinterpret_cast<uint32_t*>(&h1);
+    pk.z = *reinterpret_cast<uint32_t*>(&h2);
+    pk.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(dst) = pk;
   }
 }
 
@@ -185,11 +199,9 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
   const int per_batch = a.m_tiles * a.n_tiles;
   u.b = tile / per_batch;
   const int rem = tile - u.b * per_batch;
-  const int mr = rem / a.n_tiles;
-  int mt = mr + a.m_rot;
-  if (mt >= a.m_tiles) mt -= a.m_tiles;
+  const int mt = rem / a.n_tiles;
   u.m0 = mt * kBM;
-  u.n0 = (rem - mr * a.n_tiles) * bn;
+  u.n0 = (rem - mt * a.n_tiles) * bn;
   u.kb0 = u.ks * a.kb_per_split;
   u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
   return u;
@@ -239,8 +251,10 @@ __device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off
   const Epilogue& e = args.epi;
   const int nvalid = min(32, args.N - n0);
   if (args.vec_ok && nvalid == 32) {
+    if (e.alpha != 1.f) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+      for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+    }
     if (e.bias != nullptr) {
 #pragma unroll
       for (int j = 0; j < 32; j += 4) {
@@ -248,20 +262,35 @@ __device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off
         v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
       }
     }
-    if (e.pre_act != nullptr) {
+    if (e.act == kActGeluSave) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) {
+        float gd[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) gelu_both(v[j + i], v[j + i], gd[i]);
+        if (e.pre_act != nullptr) store8(e.pre_act, e.pre_dtype, off + j, gd);
+      }
+    } else if (e.pre_act != nullptr) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8) store8(e.pre_act, e.pre_dtype, off + j, v + j);
     }
     if (e.act == kActGelu) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-    } else if (e.act == kActGeluGrad) {
+    } else if (e.act == kActGeluGrad || e.act == kActMulAux || e.act == kActSoftmaxBwd) {
+      const float rv = e.act == kActSoftmaxBwd ? e.alpha * e.rowvec[off / e.rv_div] : 0.f;
+      float g[32];
 #pragma unroll
-      for (int j = 0; j < 32; j += 8) {
-        float g[8];
-        load8(e.aux, e.aux_dtype, off + j, g);
+      for (int j = 0; j < 32; j += 8) load8(e.aux, e.aux_dtype, off + j, g + j);
+      if (e.act == kActMulAux) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_f(g[i]);
+        for (int j = 0; j < 32; ++j) v[j] *= g[j];
+      } else if (e.act == kActSoftmaxBwd) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = g[j] * (v[j] - rv);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(g[j]);
       }
     }
     if (e.resid != nullptr) {
@@ -291,59 +320,125 @@ __device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off
   }
 }
 
-// Epilogue math on CW values of one output row starting at column n0; `off` is the
-// element offset of (m, n0) for aux/resid/accumulate loads (valid when row_ok).
-// A requested pre-activation store goes through the staging buffer and tmP.
+// One 16-B raw chunk holds 8 bf16 or 4 fp32 values; element j of a CW-wide row segment
+// (CW = 64 bf16 or 32 fp32: 8 chunks either way).
 template <int CW>
-__device__ __forceinline__ void epi_math_tma(const TcArgs& args, long long off, int n0, float* v,
-                                             bool row_ok, const CUtensorMap* tmP, uint8_t* buf,
-                                             int lane, int c0, int c1, int c2, int c3, int c4) {
+__device__ __forceinline__ float raw_at(const uint4 (&raw)[8], int j) {
+  if (CW == 32) {
+    return __uint_as_float(reinterpret_cast<const uint32_t*>(&raw[j >> 2])[j & 3]);
+  } else {
+    const uint32_t w = reinterpret_cast<const uint32_t*>(&raw[j >> 3])[(j & 7) >> 1];
+    return __uint_as_float((j & 1) ? (w & 0xFFFF0000u) : (w << 16));
+  }
+}
+
+template <int CW>
+__device__ __forceinline__ void load_raw(const void* base, int dtype, long long off, uint4 (&raw)[8]) {
+  const uint4* p = reinterpret_cast<const uint4*>(static_cast<const char*>(base) +
+                                                  off * (dtype == kF32 ? 4 : 2));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) raw[q] = __ldg(p + q);
+}
+
+// Element j (0..CW) of row `lane` of a swizzled [32][128 B] chunk buffer.
+template <int CW>
+__device__ __forceinline__ float smem_at(const uint8_t* xbuf, int lane, int j) {
+  constexpr int VPC = CW == 32 ? 4 : 8;
+  const uint8_t* p = xbuf + lane * 128 + (((j / VPC) ^ (lane & 7)) << 4);
+  if (CW == 32) return reinterpret_cast<const float*>(p)[j % VPC];
+  const uint16_t u = reinterpret_cast<const uint16_t*>(p)[j % VPC];
+  return __uint_as_float(static_cast<uint32_t>(u) << 16);
+}
+
+// Epilogue math on 32 values of one output row starting at column n0 (half h of a CW-wide
+// chunk); `off` is the element offset of (m, n0) (valid when row_ok). `xbuf`: the chunk's
+// aux (x_tma 1) or residual (x_tma 2) values, TMA-loaded into shared memory. `rv`: the
+// row's kActSoftmaxBwd value, alpha * rowvec[row]. A pre-activation output is written
+// with direct 16-B stores (the staging buffer carries the main output only).
+template <int CW>
+__device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, int n0, float (&v)[32],
+                                           bool row_ok, bool vec, uint8_t* xbuf, int lane,
+                                           int h, float rv) {
   const Epilogue& e = args.epi;
-  const bool full = n0 + CW <= args.N;
-  const int nvalid = min(CW, args.N - n0);
+  const int nvalid = min(32, args.N - n0);
+  // the pre-activation pass already wrote gelu(alpha * acc + bias) back to TMEM
+  const bool applied = args.pre_tma && e.pre_act != nullptr && e.act == kActGeluSave;
+  if (e.alpha != 1.f && !applied) {
 #pragma unroll
-  for (int j = 0; j < CW; ++j) v[j] *= e.alpha;
-  if (e.bias != nullptr) {
-    if (full) {
+    for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+  }
+  if (e.bias != nullptr && !applied) {
+    if (vec) {
 #pragma unroll
-      for (int j = 0; j < CW; j += 4) {
+      for (int j = 0; j < 32; j += 4) {
         const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + n0 + j));
         v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < CW; ++j)
+      for (int j = 0; j < 32; ++j)
         if (j < nvalid) v[j] += e.bias[n0 + j];
     }
   }
-  if (e.pre_act != nullptr) {
-    staging_acquire(lane);
-    stage_row<CW>(buf, lane, v);
-    store_staged(tmP, buf, lane, c0, c1, c2, c3, c4);
-  }
-  const bool vec = full && row_ok && args.vec_ok;
-  if (e.act == kActGelu) {
+  if (e.pre_act != nullptr && args.pre_tma) {
+    // stored by the separate staging pass of epi_tile_tma
+  } else if (e.pre_act != nullptr && row_ok) {
+    if (e.act == kActGeluSave) {
 #pragma unroll
-    for (int j = 0; j < CW; ++j) v[j] = gelu_f(v[j]);
-  } else if (e.act == kActGeluGrad && row_ok) {
-    if (vec) {
+      for (int j = 0; j < 32; j += 8) {
+        float gd[8];
 #pragma unroll
-      for (int j = 0; j < CW; j += 8) {
-        float g[8];
-        load8(e.aux, e.aux_dtype, off + j, g);
+        for (int i = 0; i < 8; ++i) gelu_both(v[j + i], v[j + i], gd[i]);
+        if (vec) {
+          store8(e.pre_act, e.pre_dtype, off + j, gd);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_f(g[i]);
+          for (int i = 0; i < 8; ++i)
+            if (j + i < nvalid) st_any(e.pre_act, e.pre_dtype, off + j + i, gd[i]);
+        }
       }
+    } else if (vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) store8(e.pre_act, e.pre_dtype, off + j, v + j);
     } else {
 #pragma unroll
-      for (int j = 0; j < CW; ++j)
-        if (j < nvalid) v[j] *= gelu_grad_f(ld_any(e.aux, e.aux_dtype, off + j));
+      for (int j = 0; j < 32; ++j)
+        if (j < nvalid) st_any(e.pre_act, e.pre_dtype, off + j, v[j]);
+    }
+  } else if (e.act == kActGeluSave) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+  }
+  if (e.act == kActGelu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+  } else if ((e.act == kActGeluGrad || e.act == kActMulAux || e.act == kActSoftmaxBwd) && row_ok) {
+    float g[32];
+    if (args.x_tma == 1) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[j] = smem_at<CW>(xbuf, lane, 32 * h + j);
+    } else if (vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) load8(e.aux, e.aux_dtype, off + j, g + j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[j] = j < nvalid ? ld_any(e.aux, e.aux_dtype, off + j) : 0.f;
+    }
+    if (e.act == kActMulAux) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= g[j];
+    } else if (e.act == kActSoftmaxBwd) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = g[j] * (v[j] - rv);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(g[j]);
     }
   }
   if (e.resid != nullptr && row_ok) {
     if (vec) {
 #pragma unroll
-      for (int j = 0; j < CW; j += 8) {
+      for (int j = 0; j < 32; j += 8) {
         float r[8];
         load8(e.resid, e.resid_dtype, off + j, r);
 #pragma unroll
@@ -351,38 +446,113 @@ __device__ __forceinline__ void epi_math_tma(const TcArgs& args, long long off, 
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < CW; ++j)
+      for (int j = 0; j < 32; ++j)
         if (j < nvalid) v[j] += ld_any(e.resid, e.resid_dtype, off + j);
     }
   }
   if (e.accumulate && row_ok) {
 #pragma unroll
-    for (int j = 0; j < CW; ++j)
+    for (int j = 0; j < 32; ++j)
       if (j < nvalid) v[j] += ld_any(e.out.base, e.out.dtype, off + j);
   }
 }
 
 template <int CW, int COLS>
 __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorMap* tmC,
-                                             const CUtensorMap* tmP, uint8_t* buf, int lane,
+                                             const CUtensorMap* tmX, uint8_t* buf, uint8_t* xbuf,
+                                             uint64_t* xbar, uint32_t& xph, int lane,
                                              uint32_t row_taddr, int ncol0, long long row_off,
                                              bool row_ok, int c1, int c2r, int c3, int c4) {
   const Epilogue& e = args.epi;
+  constexpr int VPC = CW == 32 ? 4 : 8;  // values per 16-B staging chunk
+  // per-row softmax-backward value (contiguous rows: row = offset / row length)
+  const float rv = (e.act == kActSoftmaxBwd && row_ok && args.ksplit == 1)
+                       ? e.alpha * __ldg(e.rowvec + row_off / e.rv_div)
+                       : 0.f;
+  auto coords = [&](int n, int& c0, int& c2) {
+    c0 = args.st_csplit ? n % args.st_csplit : n;
+    c2 = c2r + (args.st_csplit ? n / args.st_csplit : 0);
+  };
+  // the first chunk's operand load overlaps the first TMEM read
+  if (args.x_tma && ncol0 < args.N && lane == 0) {
+    int c0, c2;
+    coords(ncol0, c0, c2);
+    ptx::mbar_arrive_expect_tx(xbar, 4096);
+    ptx::tma_load_5d(xbuf, tmX, xbar, c0, c1, c2, c3, c4);
+  }
 #pragma unroll 1
   for (int cc = 0; cc < COLS / CW; ++cc) {
-    float v[CW];
-    ptx::tmem_ld32(row_taddr + cc * CW, *reinterpret_cast<float(*)[32]>(v));
-    if (CW == 64) ptx::tmem_ld32(row_taddr + cc * CW + 32, *reinterpret_cast<float(*)[32]>(v + 32));
     const int n = ncol0 + cc * CW;
-    if (n >= args.N) continue;  // warp-uniform
-    const int c0 = args.st_csplit ? n % args.st_csplit : n;
-    const int c2 = c2r + (args.st_csplit ? n / args.st_csplit : 0);
-    if (args.ksplit == 1) {
-      const long long off = row_off + (e.out.csplit ? (n % e.out.csplit) + (n / e.out.csplit) * e.out.s_hi : n);
-      epi_math_tma<CW>(args, off, n, v, row_ok, tmP, buf, lane, c0, c1, c2, c3, c4);
+    const bool live = n < args.N;  // warp-uniform
+    const long long off =
+        row_off + (e.out.csplit ? (n % e.out.csplit) + (n / e.out.csplit) * e.out.s_hi : n);
+    const bool vec = live && args.ksplit == 1 && row_ok && args.vec_ok && n + CW <= args.N;
+    if (args.pre_tma && live && args.ksplit == 1) {
+      // pre-activation pass: alpha * acc + bias (or gelu'(x) for kActGeluSave) staged and
+      // TMA-stored, then the main pass re-reads TMEM
+      int c0p, c2p;
+      coords(n, c0p, c2p);
+      staging_acquire(lane);
+#pragma unroll
+      for (int h = 0; h < CW / 32; ++h) {
+        float v[32];
+        ptx::tmem_ld32(row_taddr + cc * CW + 32 * h, v);
+        const int nh = n + 32 * h;
+        if (e.alpha != 1.f) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
+        }
+        if (e.bias != nullptr) {
+          if (nh + 32 <= args.N && args.vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + nh + j));
+              v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nh + j < args.N) v[j] += e.bias[nh + j];
+          }
+        }
+        if (e.act == kActGeluSave) {
+          // gelu goes back to TMEM for the main pass, gelu' to the staging buffer
+          float g[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gelu_both(v[j], g[j], v[j]);
+          ptx::tmem_st32(row_taddr + cc * CW + 32 * h, g);
+        }
+#pragma unroll
+        for (int q = 0; q < 32 / VPC; ++q) stage_chunk<CW>(buf, lane, h * (32 / VPC) + q, v + VPC * q);
+      }
+      store_staged(tmX, buf, lane, c0p, c1, c2p, c3, c4);
     }
     staging_acquire(lane);
-    stage_row<CW>(buf, lane, v);
+    if (args.x_tma && live) {
+      ptx::mbar_wait(xbar, xph);
+      xph ^= 1;
+    }
+#pragma unroll
+    for (int h = 0; h < CW / 32; ++h) {
+      float v[32];
+      ptx::tmem_ld32(row_taddr + cc * CW + 32 * h, v);
+      if (live && args.ksplit == 1)
+        epi_math32<CW>(args, off + 32 * h, n + 32 * h, v, row_ok, vec, xbuf, lane, h, rv);
+#pragma unroll
+      for (int q = 0; q < 32 / VPC; ++q) stage_chunk<CW>(buf, lane, h * (32 / VPC) + q, v + VPC * q);
+    }
+    if (!live) continue;
+    // every lane has read the operand chunk: fetch the next one during this store
+    __syncwarp();
+    const int nn = n + CW;
+    if (args.x_tma && cc + 1 < COLS / CW && nn < args.N && lane == 0) {
+      int c0n, c2n;
+      coords(nn, c0n, c2n);
+      ptx::mbar_arrive_expect_tx(xbar, 4096);
+      ptx::tma_load_5d(xbuf, tmX, xbar, c0n, c1, c2n, c3, c4);
+    }
+    int c0, c2;
+    coords(n, c0, c2);
     store_staged(tmC, buf, lane, c0, c1, c2, c3, c4);
   }
 }
@@ -408,12 +578,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + S * kABytes;
   uint8_t* smem_stage = smem + S * kStageBytes;  // 8 epilogue warps x 4 KB, 1024-aligned
-  uint64_t* full_bar =
-      reinterpret_cast<uint64_t*>(smem + S * kStageBytes + (args.tma_store ? kEpiWarps * 4096 : 0));
+  uint8_t* smem_x = smem_stage + kEpiWarps * 4096;  // operand chunks (x_tma)
+  const int staging = args.tma_store ? kEpiWarps * 4096 * (args.x_tma ? 2 : 1) : 0;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStageBytes + staging);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* x_bar = tempty_bar + 2;  // one per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_bar + kEpiWarps);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -430,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&tfull_bar[s], 1);
       ptx::mbar_init(&tempty_bar[s], kEpiWarps);
     }
+    for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(&x_bar[w], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -444,29 +617,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       OpPos pa, pb;
-      bool ag_ok = false;
       for (int t = blockIdx.x; t < units; t += gridDim.x) {
         const Unit u = decode_unit(args, t, BN);
-        const CUtensorMap* amap = &tmA;
-        int arow = u.m0;
-        if (args.ag_rows) {
-          const int blk = u.m0 / args.ag_rows;
-          amap = &rsm.ag[blk];
-          arow = u.m0 - blk * args.ag_rows;
-          if (blk != args.ag_own && !ag_ok) {
-            // the peer's comm warps (one per CTA) have pushed its rows
-            const uint32_t epoch = *args.rs_epoch;
-            for (int c = 0; c < static_cast<int>(gridDim.x); ++c) ptx::wait_epoch(args.ag_wait + c, epoch);
-            ptx::fence_proxy_async_global();
-            ag_ok = true;
-          }
-        }
-        op_init(args.a, pa, arow, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
+        op_init(args.a, pa, u.m0, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
         op_init(args.b, pb, u.n0, B_MN ? BN / 64 : 1, u.kb0 * kBK, u.b);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[s], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          op_issue<kBM>(amap, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
+          op_issue<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
           op_issue<BN>(&tmB, args.b, pb, smem_b + s * kBBytes, &full_bar[s]);
           op_advance(args.a, pa);
           op_advance(args.b, pb);
@@ -516,35 +674,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kCommWarp) {
-    if (args.ag_rows) {
-      // ---------------- all-gather push: this CTA's 1/grid of the shard goes to the
-      // peer's gathered buffer over NVLink (and to the local one when it is kept), then
-      // a per-CTA arrival flag is raised on the peer (release, system scope)
-      constexpr int U = 8;
-      const long long nvec = args.ag_bytes / 16;
-      const long long lo = nvec * blockIdx.x / gridDim.x, hi = nvec * (blockIdx.x + 1) / gridDim.x;
-      const uint4* src = reinterpret_cast<const uint4*>(args.ag_src);
-      uint4* dst = reinterpret_cast<uint4*>(args.ag_peer_dst);
-      uint4* own = reinterpret_cast<uint4*>(args.ag_own_dst);
-      for (long long i0 = lo + lane; i0 < hi; i0 += 32 * U) {
-        uint4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (i0 + 32 * u < hi) v[u] = src[i0 + 32 * u];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (i0 + 32 * u < hi) {
-            dst[i0 + 32 * u] = v[u];
-            if (own) own[i0 + 32 * u] = v[u];
-          }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_system();
-        ptx::st_release_sys(args.ag_signal + blockIdx.x, *args.rs_epoch);
-      }
-    }
   } else {
     // ---------------- epilogue warps 2..9: lane quarter = warp % 4, column half = (warp-2)/4
     const int quarter = warp & 3;
@@ -554,8 +683,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const Epilogue& e = args.epi;
     if (args.tma_store) {
       uint8_t* buf = smem_stage + (warp - 2) * 4096;
-      const bool need_off =
-          args.ksplit == 1 && (e.aux != nullptr || e.resid != nullptr || e.accumulate);
+      uint8_t* xbuf = smem_x + (warp - 2) * 4096;
+      uint64_t* xbar = &x_bar[warp - 2];
+      uint32_t xph = 0;
+      const bool need_off = args.ksplit == 1 && (e.aux != nullptr || e.resid != nullptr ||
+                                                 e.accumulate || e.rowvec != nullptr ||
+                                                 e.pre_act != nullptr);
       const uint32_t epoch = args.rs_P ? *args.rs_epoch : 0u;
       uint32_t entered_mask = 0;
       for (int t = blockIdx.x; t < units; t += gridDim.x) {
@@ -587,11 +720,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                    (static_cast<uint32_t>(quarter * 32) << 16) + half * kColsPerWarp;
         const int ncol0 = u.n0 + half * kColsPerWarp;
         if (args.cw == 32)
-          epi_tile_tma<32, kColsPerWarp>(args, cmap, &tmP, buf, lane, row_taddr, ncol0, row_off,
-                                         row_ok, c1, c2r, c3, c4);
+          epi_tile_tma<32, kColsPerWarp>(args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr,
+                                         ncol0, row_off, row_ok, c1, c2r, c3, c4);
         else
           epi_tile_tma<(kColsPerWarp >= 64 ? 64 : 32), kColsPerWarp>(
-              args, cmap, &tmP, buf, lane, row_taddr, ncol0, row_off, row_ok, c1, c2r, c3, c4);
+              args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr, ncol0, row_off, row_ok, c1,
+              c2r, c3, c4);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
@@ -767,11 +901,11 @@ CUtensorMap make_operand_map(const View& v, long long rows, long long cols, int 
 // batch-hi), box [32 rows][128 B], 128B swizzle. Returns false when the view is not
 // TMA-addressable (the kernel then stores directly from registers).
 bool make_store_map(const View& v, long long rows, long long cols, int batch, int cw,
-                    CUtensorMap* map) {
+                    CUtensorMap* map, int box_rows = 32) {
   const long long es = v.dtype == kF32 ? 4 : 2;
   if (v.sc != 1 || reinterpret_cast<uintptr_t>(v.base) % 16) return false;
   if (v.rsplit && v.csplit) return false;
-  if (v.rsplit && v.rsplit % 32) return false;
+  if (v.rsplit && v.rsplit % box_rows) return false;
   if (v.csplit && v.csplit % cw) return false;
   for (long long s : {v.sr, v.s_hi, v.sb_lo, v.sb_hi})
     if ((s * es) % 16) return false;
@@ -789,7 +923,7 @@ bool make_store_map(const View& v, long long rows, long long cols, int batch, in
                            static_cast<cuuint64_t>(v.sb_lo ? v.sb_lo * es : fb),
                            static_cast<cuuint64_t>(v.sb_hi ? v.sb_hi * es : fb)};
   if (rows == 1 || rlo == 1) strides[0] = std::max<cuuint64_t>(strides[0], 16);
-  cuuint32_t box[5] = {static_cast<cuuint32_t>(cw), 32, 1, 1, 1};
+  cuuint32_t box[5] = {static_cast<cuuint32_t>(cw), static_cast<cuuint32_t>(box_rows), 1, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   std::memset(map, 0, sizeof(*map));
   const CUresult r = encode_fn()(
@@ -804,11 +938,11 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
                const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
                cudaStream_t stream) {
   constexpr int kStageBytes = (kBM + BN) * kBK * 2;
-  const int staging = args.tma_store ? kEpiWarps * 4096 : 0;
+  const int staging = args.tma_store ? kEpiWarps * 4096 * (args.x_tma ? 2 : 1) : 0;
   int stages = (kSmemBudget - 1024 - 256 - staging) / kStageBytes;
   stages = std::min(stages, 8);
   args.stages = stages;
-  const int smem = 1024 + stages * kStageBytes + staging + (2 * stages + 4) * 8 + 16;
+  const int smem = 1024 + stages * kStageBytes + staging + (2 * stages + 4 + kEpiWarps) * 8 + 16;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -877,6 +1011,19 @@ int pick_ksplit(long long M, long long N, int tiles, int k_blocks, int batch, in
 }
 
 }  // namespace
+
+CUtensorMap tc_operand_map(const View& v, long long rows, long long cols, int batch, int box_rows,
+                           int* mn_major) {
+  TcOperand op;
+  CUtensorMap m = make_operand_map(v, rows, cols, batch, box_rows, &op);
+  if (mn_major) *mn_major = op.mn_major;
+  return m;
+}
+
+bool tc_store_map(const View& v, long long rows, long long cols, int batch, int box_cols,
+                  int box_rows, CUtensorMap* map) {
+  return make_store_map(v, rows, cols, batch, box_cols, map, box_rows);
+}
 
 int tc_pick_bn(long long M, long long N, int batch, int num_sms) {
   (void)M;
@@ -979,11 +1126,17 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.cw = sv.dtype == kF32 ? 32 : 64;
   bool tma = !std::getenv("C3D_NO_TMA_STORE") && args.cw <= bn / 2 &&
              make_store_map(sv, p.M, p.N, sbatch, args.cw, &mc);
-  if (tma && args.ksplit == 1 && p.epi.pre_act) {
-    View pv = p.epi.out;
-    pv.base = p.epi.pre_act;
-    pv.dtype = p.epi.pre_dtype;
-    tma = pv.dtype == sv.dtype && make_store_map(pv, p.M, p.N, p.batch, args.cw, &mp);
+  // epilogue operand (aux or residual, same layout as the output) by TMA when the output
+  // goes out by TMA; the pre-activation output is written directly
+  if (tma && args.ksplit == 1 && !std::getenv("C3D_NO_X_TMA")) {
+    View xv = p.epi.out;
+    if (p.epi.pre_act && p.epi.pre_dtype == p.epi.out.dtype) {
+      xv.base = p.epi.pre_act;
+      if (make_store_map(xv, p.M, p.N, p.batch, args.cw, &mp)) args.pre_tma = 1;
+    } else if (p.epi.aux && p.epi.aux_dtype == p.epi.out.dtype) {
+      xv.base = const_cast<void*>(p.epi.aux);
+      if (make_store_map(xv, p.M, p.N, p.batch, args.cw, &mp)) args.x_tma = 1;
+    }
   }
   RsMaps rsm;
   std::memset(&rsm, 0, sizeof(rsm));
@@ -1008,27 +1161,6 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     args.rs_done_offset = p.rs.done_offset;
     args.rs_epoch = p.rs.epoch;
     sv = View();
-  }
-  if (p.ag.block_rows > 0) {
-    if (p.batch != 1 || p.ag.block_rows % kBM || p.M != 2 * p.ag.block_rows ||
-        args.ksplit != 1 || p.rs.P < 2 || (p.ag.block_rows * p.K * 2) % 16 ||
-        reinterpret_cast<uintptr_t>(p.ag.a_block[p.ag.own]) % 16)
-      throw std::runtime_error("tc_gemm: fused all-gather unsupported");
-    for (int k = 0; k < 2; ++k) {
-      View v = p.a;
-      v.base = const_cast<void*>(p.ag.a_block[k]);
-      TcOperand op;
-      rsm.ag[k] = make_operand_map(v, p.ag.block_rows, p.K, 1, kBM, &op);
-    }
-    args.ag_rows = static_cast<int>(p.ag.block_rows);
-    args.ag_own = p.ag.own;
-    args.m_rot = p.ag.own * static_cast<int>(p.ag.block_rows / kBM);
-    args.ag_src = static_cast<const char*>(p.ag.a_block[p.ag.own]);
-    args.ag_peer_dst = static_cast<char*>(p.ag.push_dst);
-    args.ag_own_dst = static_cast<char*>(p.ag.own_dst);
-    args.ag_bytes = p.ag.block_rows * p.K * 2;
-    args.ag_signal = p.ag.signal;
-    args.ag_wait = p.ag.wait;
   }
   args.tma_store = tma ? 1 : 0;
   args.st_rsplit = static_cast<int>(sv.rsplit);

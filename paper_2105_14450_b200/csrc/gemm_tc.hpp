@@ -1,5 +1,6 @@
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "gemm.hpp"
@@ -16,6 +17,14 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
 // is TMA-storable with whole tiles; `tc_gemm_grid` is the CTA count (one done flag each).
 bool tc_gemm_rs_supported(const GemmProblem& p, int bn);
 int tc_gemm_grid(const GemmProblem& p, int bn, int num_sms);
+
+// TMA maps for the other tcgen05 kernels (attention.cu): a 5-D operand map (box
+// 64 K-columns x box_rows rows, 128B swizzle; MN-major views get 64 x 64 boxes) and a
+// store/load map with an explicit box (128B swizzle).
+CUtensorMap tc_operand_map(const View& v, long long rows, long long cols, int batch, int box_rows,
+                           int* mn_major);
+bool tc_store_map(const View& v, long long rows, long long cols, int batch, int box_cols,
+                  int box_rows, CUtensorMap* map);
 
 // SIMT fp32 path: any view, fp32 or bf16 operands, fp32 FMA in ascending k.
 void simt_gemm_launch(const GemmProblem& p, cudaStream_t stream);

@@ -50,6 +50,56 @@ __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int
     st_any(dst, ddt, t, ld_any(src, sdt, t));
 }
 
+// y = gelu(x); x <- gelu'(x) in place (the MLP's saved pre-activation becomes the
+// factor its backward multiplies by). Vector path: 8 bf16 / 4+4 fp32 per thread.
+__global__ void gelu_save_kernel(void* x, int xdt, void* y, int ydt, int64_t n, int vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (vec) {
+    for (int64_t t = t0; t < n / 8; t += stride) {
+      float v[8], g[8], d[8];
+      if (xdt == kBF16) {
+        const uint4 q = reinterpret_cast<const uint4*>(x)[t];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          v[2 * i] = f.x;
+          v[2 * i + 1] = f.y;
+        }
+      } else {
+        const float4 a = reinterpret_cast<const float4*>(x)[2 * t];
+        const float4 b = reinterpret_cast<const float4*>(x)[2 * t + 1];
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) gelu_both(v[i], g[i], d[i]);
+      auto put = [&](void* base, int dt, const float* w) {
+        if (dt == kBF16) {
+          uint4 q;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+          reinterpret_cast<uint4*>(base)[t] = q;
+        } else {
+          reinterpret_cast<float4*>(base)[2 * t] = make_float4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<float4*>(base)[2 * t + 1] = make_float4(w[4], w[5], w[6], w[7]);
+        }
+      };
+      put(y, ydt, g);
+      put(x, xdt, d);
+    }
+    return;
+  }
+  for (int64_t t = t0; t < n; t += stride) {
+    float g, d;
+    gelu_both(ld_any(x, xdt, t), g, d);
+    st_any(y, ydt, t, g);
+    st_any(x, xdt, t, d);
+  }
+}
+
 __global__ void mul_cols_kernel(const void* a, int adt, const float* b, void* c, int cdt,
                                 int64_t rows, int64_t cols) {
   const int64_t n = rows * cols;
@@ -227,6 +277,16 @@ void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStre
   if (n == 0) return;
   convert_kernel<<<grid_for(n), 256, 0, s>>>(src, sdt, dst, ddt, n);
   check_launch("convert");
+}
+
+void k_gelu_save(void* x, int xdt, void* y, int ydt, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  const bool vec = n % 8 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(y) % 16 == 0;
+  const int64_t work = vec ? n / 8 : n;
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 148 * 16));
+  gelu_save_kernel<<<blocks, 256, 0, s>>>(x, xdt, y, ydt, n, vec ? 1 : 0);
+  check_launch("gelu_save");
 }
 
 void k_mul_cols(const void* a, int adt, const float* b, void* c, int cdt, int64_t rows,

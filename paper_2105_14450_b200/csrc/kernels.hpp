@@ -23,6 +23,8 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
               float* out, cudaStream_t s);
 
 void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
+// y = gelu(x), x <- gelu'(x) (n elements, in place on x).
+void k_gelu_save(void* x, int xdt, void* y, int ydt, int64_t n, cudaStream_t s);
 
 // c[r][col] = a[r][col] * b[col] (mul_vec_fwd, cube3d/ops3d.hpp:391-393).
 void k_mul_cols(const void* a, int adt, const float* b, void* c, int cdt, int64_t rows,
@@ -63,6 +65,9 @@ void k_softmax_bwd_rowdot(const float* dp, const void* p, int pdt, int64_t rows,
                           float* rowdot, cudaStream_t s);
 void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                       const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s);
+// Row dot products sum_d dO*O of packed [bi][q][head][dh] buffers (softmax backward).
+void k_attn_rowdot(const void* d_o, const void* o, int dt, int64_t nslices, int64_t S, int64_t H,
+                   int64_t dh, int64_t sb_hi, float* out, cudaStream_t s);
 void k_softmax_bwd_fused(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                          float scale, void* ds, int dsdt, cudaStream_t s);
 

@@ -12,6 +12,8 @@
 #include "kernels.hpp"
 #include "nn.hpp"
 
+#include <cstdlib>
+
 namespace c3d {
 
 namespace {
@@ -343,7 +345,18 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
   const int64_t srows = static_cast<int64_t>(nslices) * a.S;
   DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s));
   S.probs = pb.get();
-  {
+  const ActGeom cg = act_geom(cube.grid(), x.batch, x.seq, cfg.hidden, qkv.group);
+  DevBuf& ctx_buf = S.keep(DevBuf(static_cast<size_t>(cg.bl * cg.sl * cg.hl) * dtype_size(dt), s));
+  Act ctx = make_act(cube, ctx_buf.get(), dt, x.batch, x.seq, cfg.hidden, qkv.group);
+  // whole key range on this rank: scores, softmax and P V in one tcgen05 kernel
+  const bool fused = a.Ps == 1 && mode != C3D_MODE_F32 && dt == kBF16 &&
+                     attn_fwd_fused(qv, qkv_view(qkv.data, dt, a, 1, false),
+                                    qkv_view(qkv.data, dt, a, 2, true),
+                                    scores_view(pb.get(), dt, a, false),
+                                    packed_out(ctx.data, dt, a, false), a.S, a.sl, a.dh, a.H,
+                                    nslices, a.scale, s);
+  if (fused) cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+  if (!fused) {
     DevBuf sc(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
     e.out = scores_view(sc.get(), kF32, a, false);
@@ -364,10 +377,7 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
     }
   }
   // context = P V, reduce-scattered back to this rank's seq block
-  const ActGeom cg = act_geom(cube.grid(), x.batch, x.seq, cfg.hidden, qkv.group);
-  DevBuf& ctx_buf = S.keep(DevBuf(static_cast<size_t>(cg.bl * cg.sl * cg.hl) * dtype_size(dt), s));
-  Act ctx = make_act(cube, ctx_buf.get(), dt, x.batch, x.seq, cfg.hidden, qkv.group);
-  {
+  if (!fused) {
     Epilogue e;
     DevBuf partial;
     if (a.Ps == 1) {
@@ -405,10 +415,30 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
 
   Gathered dcf = gather(cube, a.seq_axis, dctx.data, rows * a.hd, dt, s);
   DevBuf dqkv_buf(static_cast<size_t>(rows * a.ld_qkv) * dtype_size(dt), s);
-  // dP = dctx_full V^T (fp32)
   const int64_t srows = static_cast<int64_t>(nslices) * a.S;
-  DevBuf dpf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
-  {
+  DevBuf dp(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s);  // dS, activation dtype
+  // whole key range on this rank (bf16): the softmax backward is fused into the dP
+  // GEMM epilogue, dS = P * (dP - D) * scale with D = rowsum(dctx * ctx) = sum_j P dP
+  const bool fused_ds = a.Ps == 1 && mode != C3D_MODE_F32 && dt == kBF16 &&
+                        !std::getenv("C3D_NO_FUSED_ATTN");
+  DevBuf dpf;
+  if (fused_ds) {
+    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
+    k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
+                  rd.as<float>(), s);
+    Epilogue e;
+    e.out = scores_view(dp.get(), dt, a, false);
+    e.alpha = a.scale;
+    e.act = kActSoftmaxBwd;
+    e.aux = S.probs;
+    e.aux_dtype = dt;
+    e.rowvec = rd.as<float>();
+    e.rv_div = a.sl;
+    gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
+               qkv_view(qkv, dt, a, 2, false), e, s);
+  } else {
+    // dP = dctx_full V^T (fp32)
+    dpf = DevBuf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
     e.out = scores_view(dpf.get(), kF32, a, false);
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
@@ -422,8 +452,8 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                packed_view(dcf.ptr, dt, a, true), e, s);
   }
   // dS = P * (dP - rowdot) * scale, rowdot summed along the seq axis
-  DevBuf dp(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s);  // dS, activation dtype
-  if (a.Ps == 1) {
+  if (fused_ds) {
+  } else if (a.Ps == 1) {
     k_softmax_bwd_fused(dpf.as<float>(), S.probs, dt, srows, a.sl, a.scale, dp.get(), dt, s);
   } else {
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
@@ -467,20 +497,26 @@ void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const Linear
              const LinearP& fc2, int& group, Act& y, MlpSaved* sv, bool own_input,
              const void* resid, cudaStream_t s, const LinearPre* fc1_pre,
              const LinearPre* fc2_pre) {
-  // mlp_fwd (cube3d/transformer.hpp:44-53); GELU fused into the FC1 epilogue.
+  // mlp_fwd (cube3d/transformer.hpp:44-53).
   MlpSaved local;
   MlpSaved& S = sv ? *sv : local;
   const int dt = x.dtype;
   const ActGeom hg = act_geom(cube.grid(), x.batch, x.seq, 4 * cfg.hidden, 1 - x.group);
   const size_t hbytes = static_cast<size_t>(hg.bl * hg.sl * hg.hl) * dtype_size(dt);
   Act h1;
-  h1.data = S.keep(DevBuf(hbytes, s)).get();
+  void* h1_data = S.keep(DevBuf(hbytes, s)).get();
   h1.dtype = dt;
   S.pre_act = S.keep(DevBuf(hbytes, s)).get();
-  LinearEpi e1;
-  e1.act = kActGelu;
-  e1.pre_act = S.pre_act;
-  linear_fwd(cube, mode, x, fc1, group, h1, &S.fc1_lin, own_input, e1, s, fc1_pre);
+  // FC1 writes the pre-activation x into S.pre_act; one elementwise pass then produces
+  // h1 = gelu(x) and leaves gelu'(x) in S.pre_act for the backward (which only
+  // multiplies, kActMulAux) -- cheaper than carrying the erf in the GEMM epilogue
+  Act pre;
+  pre.data = S.pre_act;
+  pre.dtype = dt;
+  linear_fwd(cube, mode, x, fc1, group, pre, &S.fc1_lin, own_input, LinearEpi{}, s, fc1_pre);
+  h1 = pre;
+  h1.data = h1_data;
+  k_gelu_save(S.pre_act, dt, h1.data, dt, static_cast<int64_t>(pre.elems()), s);
   LinearEpi e2;
   e2.resid = resid;
   linear_fwd(cube, mode, h1, fc2, group, y, &S.fc2_lin, false, e2, s, fc2_pre);

@@ -116,7 +116,7 @@ void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group
                 LinearSaved* saved, bool own_input, const LinearEpi& extra, cudaStream_t s,
                 const LinearPre* pre = nullptr);
 void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, const LinearP& p,
-                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s,
+                Act* dx, Mat* dw, const Vec* db, const void* dx_gelu_aux, cudaStream_t s,  // aux: gelu'(x) values (kActMulAux)
                 const Operand* wg = nullptr, const LinearSinks* sinks = nullptr);
 
 // `gblock`/`bblock`: gamma/beta already expanded (layer-level); `colsum_sink`: write

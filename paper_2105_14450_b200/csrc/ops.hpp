@@ -18,6 +18,13 @@ void prof_enable(bool on);
 void prof_read(double* ms, double* flops, long long* launches);
 void prof_read_comm(double* ms, double* bytes, long long* calls);
 
+// Fused attention core (attention.cu) for slices holding the whole key range: scores
+// in TMEM, softmax, probabilities saved to `probs`, context = P V into `ctx`. Returns
+// false (nothing launched) when the shapes are outside its limits.
+bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
+                    int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
+                    cudaStream_t s);
+
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
                 const View& b, const Epilogue& e, cudaStream_t s);
@@ -60,14 +67,6 @@ Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype
 // apply -- the decision is identical on every rank -- and the caller falls back.
 bool gemm_reduce_scatter(Cube& cube, int mode, int axis, int64_t M, int64_t N, int64_t K,
                          const View& a, const View& b, const Epilogue& post, cudaStream_t s);
-// All-gather -> GEMM -> reduce-scatter with both transfers overlapped (lines of 2):
-// the shard (rows x K, K-major bf16) goes to the all-gather peer by copy engine while
-// the GEMM runs over the local rows; the peer's rows follow once they land; output row
-// blocks are reduce-scattered along rs_axis in the epilogue. `gathered` (optional)
-// receives the full gathered operand [2][rows][K].
-bool ag_gemm_rs(Cube& cube, int mode, int ag_axis, int rs_axis, const void* a_shard, int a_dtype,
-                int64_t rows, int64_t K, const View& b, int64_t N, const Epilogue& post,
-                Gathered* gathered, cudaStream_t s);
 
 
 // expand_diagonal (cube3d/ops3d.hpp:291-310): fp32 column block of length len/p_out

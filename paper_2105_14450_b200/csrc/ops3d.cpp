@@ -1,7 +1,8 @@
 // 3-D matmul and matrix-vector operators (cube3d/ops3d.hpp), executed per rank
 // as: NCCL all-gathers along the operand axes -> one local GEMM whose operand
 // views address the gathered buffers in place (no gather_cols reorder, no
-// transposes) -> NCCL reduce-scatter along the result axis -> fused epilogue.
+// transposes) -> reduce-scatter along the result axis (fused into the GEMM epilogue over
+// NVLink peer memory when the shapes allow, fused.cu) -> fused epilogue.
 #include <string>
 
 #include "common.hpp"
@@ -330,19 +331,6 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
     bv.s_hi = b_hi;
   }
   c = make_mat(cube, c.data, c.dtype, a.grows, b.gcols, kOutput, d.swapped());
-  if (Pin > 1 && Pout > 1) {
-    Epilogue f;
-    f.out = out_view(c.data, c.dtype, c.cols);
-    f.bias = le.bias;
-    f.act = le.act;
-    f.pre_act = le.pre_act;
-    f.pre_dtype = c.dtype;
-    f.resid = le.resid;
-    f.resid_dtype = c.dtype;
-    // gather, product and reduce-scatter as one overlapped operator over NVLink
-    if (ag_gemm_rs(cube, mode, d.in, d.out, a.data, a.dtype, a.rows, a.cols, bv, Ng, f, keep_a, s))
-      return;
-  }
   Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
   View av = kmajor(af.ptr, a.dtype, a.cols);
   if (keep_a) *keep_a = std::move(af);  // buffer (if any) outlives this call
@@ -404,27 +392,13 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
       bv.csplit = b.cols;
       bv.s_hi = b_hi;
     }
-    bool fused = false;
-    if (Pin > 1 && Pout > 1) {
-      Epilogue f;
-      f.out = out_view(da->data, da->dtype, da->cols);
-      if (da_gelu_aux) {
-        f.act = kActGeluGrad;
-        f.aux = da_gelu_aux;
-        f.aux_dtype = da->dtype;
-      }
-      fused = ag_gemm_rs(cube, mode, d.out, d.in, dc.data, dc.dtype, dc.rows, Kc, bv, b.rows, f,
-                         want_db ? &dcf : nullptr, s);
-      have_dcf = fused && want_db;
-    }
-    if (!fused) need_dcf();
+    need_dcf();
     View av = kmajor(dcf.ptr, dc.dtype, Kc);
     Epilogue e;
-    if (fused) {
-    } else if (Pin == 1) {
+    if (Pin == 1) {
       e.out = out_view(da->data, da->dtype, da->cols);
       if (da_gelu_aux) {
-        e.act = kActGeluGrad;
+        e.act = kActMulAux;
         e.aux = da_gelu_aux;
         e.aux_dtype = da->dtype;
       }
@@ -433,7 +407,7 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
       Epilogue f;
       f.out = out_view(da->data, da->dtype, da->cols);
       if (da_gelu_aux) {
-        f.act = kActGeluGrad;
+        f.act = kActMulAux;
         f.aux = da_gelu_aux;
         f.aux_dtype = da->dtype;
       }

@@ -103,6 +103,21 @@ __global__ void bwd_fused_kernel(const float* sc, const void* p, int pdt, int64_
 
 #undef ROW_PROLOGUE
 
+// D[b*S + q] = sum_d dO[b][q][d] * O[b][q][d] over packed [bi][q][head][dh] context
+// buffers: the softmax-backward row dot product sum_j P_ij dP_ij (dP = dO V^T, O = P V).
+__global__ void attn_rowdot_kernel(const void* d_o, const void* o, int dt, int64_t rows,
+                                   int64_t S, int64_t H, int64_t dh, int64_t sb_hi, float* out) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarps) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const int64_t b = r / S, q = r - (r / S) * S;
+  const int64_t base = (b / H) * sb_hi + q * (H * dh) + (b % H) * dh;
+  float acc = 0.f;
+  for (int64_t d = lane; d < dh; d += 32) acc += ld_any(d_o, dt, base + d) * ld_any(o, dt, base + d);
+  acc = wsum(acc);
+  if (lane == 0) out[r] = acc;
+}
+
 }  // namespace
 
 #define LAUNCH_ROWS(kern, name, ...)                                               \
@@ -134,6 +149,13 @@ void k_softmax_bwd_rowdot(const float* dp, const void* p, int pdt, int64_t rows,
 void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                       const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s) {
   LAUNCH_ROWS(bwd_ds_kernel, "softmax_bwd_ds", dp, p, pdt, rows, cols, rowdot, scale, ds, dsdt);
+}
+void k_attn_rowdot(const void* d_o, const void* o, int dt, int64_t nslices, int64_t S, int64_t H,
+                   int64_t dh, int64_t sb_hi, float* out, cudaStream_t s) {
+  const int64_t rows = nslices * S;
+  if (rows == 0) return;
+  attn_rowdot_kernel<<<blocks_for(rows), kWarps * 32, 0, s>>>(d_o, o, dt, rows, S, H, dh, sb_hi, out);
+  check_launch("attn_rowdot");
 }
 void k_softmax_bwd_fused(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                          float scale, void* ds, int dsdt, cudaStream_t s) {

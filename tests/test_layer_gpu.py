@@ -74,9 +74,10 @@ def compare_bf16(y, dx, gr, gp, x, dy, b, s, n):
         check_bf16(gr[f], getattr(Go, f).reshape(shp), f, getattr(Ge, f).reshape(shp))
 
 
-@pytest.mark.parametrize("shape", [(4, 128, 4, 256), (2, 512, 16, 1024)])
+@pytest.mark.parametrize("shape", [(4, 128, 4, 256), (2, 256, 4, 256), (2, 512, 16, 1024)])
 def test_layer_bf16_tensor_core_shapes(cube, shape):
-    """Shapes where every GEMM takes the tcgen05 path (dh = 64), vs the oracle."""
+    """Shapes where every GEMM takes the tcgen05 path (dh = 64), vs the oracle; s = 256 and
+    512 also take the fused attention kernel (scores in TMEM)."""
     b, s, n, h = shape
     r = O.Rng(99)
     P = O.init_layer_params(h, 99)
@@ -87,6 +88,24 @@ def test_layer_bf16_tensor_core_shapes(cube, shape):
     y, dx, gr = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
     assert c3.launch_count() > launches0
     compare_bf16(y, dx, gr, gp, x, dy, b, s, n)
+
+
+def test_fused_attention_matches_unfused(cube, monkeypatch):
+    """The fused attention kernel (scores/softmax/PV in one tcgen05 kernel) against the
+    unfused path (scores GEMM -> softmax kernel -> P V GEMM) on the same inputs."""
+    b, s, n, h = 2, 512, 8, 512
+    r = O.Rng(17)
+    P = O.init_layer_params(h, 17)
+    gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
+    x = bf16_round(O.random_matrix(b * s, h, r))
+    dy = bf16_round(O.random_matrix(b * s, h, r))
+    fused = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    monkeypatch.setenv("C3D_NO_FUSED_ATTN", "1")
+    plain = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    assert O.normwise_err(fused[0], plain[0]) < 2e-3
+    assert O.normwise_err(fused[1], plain[1]) < 5e-3
+    for f in O.FIELDS:
+        assert O.normwise_err(fused[2][f], plain[2][f]) < 5e-3, f
 
 
 def test_layer_fp32_mid_shape(cube):
