@@ -133,6 +133,16 @@ void Cube::all_gather(int axis, const void* send, void* recv, size_t count, int 
   charge(C3D_ALL_GATHER, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
 }
 
+void Cube::all_gather_sym(int axis, const void* send, const SymBuf& recv, size_t count, int dtype,
+                          cudaStream_t s) {
+  const int p = extent(axis);
+  if (p == 1 || !symm_) fail(C3D_ERR_INTERNAL, "all_gather_sym needs the peer transport");
+  Timed t(s, C3D_ALL_GATHER, static_cast<double>(p) * count * dtype_size(dtype));
+  symm_->all_gather_direct(line_[axis], coords_[axis], send, recv.offset(), count, dtype, num_sms_,
+                           s);
+  charge(C3D_ALL_GATHER, static_cast<uint64_t>(p - 1) * count, static_cast<uint64_t>(p - 1) * count);
+}
+
 void Cube::reduce_scatter(int axis, const void* send, void* recv, size_t count, int dtype,
                           cudaStream_t s) {
   const int p = extent(axis);

@@ -98,6 +98,9 @@ class Cube {
   // Collectives along one axis line. Counts are in elements.
   void all_gather(int axis, const void* send, void* recv, size_t count, int dtype,
                   cudaStream_t s);
+  // Same into a symmetric arena buffer (peer-memory transport only).
+  void all_gather_sym(int axis, const void* send, const SymBuf& recv, size_t count, int dtype,
+                      cudaStream_t s);
   // send holds extent(axis)*count elements; recv receives this rank's count-slice of the sum.
   void reduce_scatter(int axis, const void* send, void* recv, size_t count, int dtype,
                       cudaStream_t s);

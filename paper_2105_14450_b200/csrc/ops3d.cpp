@@ -9,6 +9,9 @@
 #include "kernels.hpp"
 #include "ops.hpp"
 
+#include <cstdlib>
+#include <memory>
+
 namespace c3d {
 
 namespace {
@@ -115,6 +118,17 @@ Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype
   if (p == 1) {
     g.ptr = shard;
     return g;
+  }
+  if (cube.symm() && std::getenv("C3D_DIRECT_AG")) {
+    // straight into a symmetric buffer: the peers push their shards over NVLink (opt-in:
+    // on this pool it measured no faster than the mailbox path, whose copy-out is cheap)
+    auto sb = std::make_unique<SymBuf>(cube.symm(), count * p * dtype_size(dtype));
+    if (sb->ok()) {
+      cube.all_gather_sym(axis, shard, *sb, count, dtype, s);
+      g.ptr = sb->local();
+      g.sym = std::move(sb);
+      return g;
+    }
   }
   g.buf = DevBuf(count * p * dtype_size(dtype), s);
   cube.all_gather(axis, shard, g.buf.get(), count, dtype, s);

@@ -33,6 +33,7 @@ struct SymmArgs {
   const char* send;
   char* recv;
   long long count, c0, n, slot_bytes;
+  int direct;  // all-gather straight into the peers' symmetric receive buffers (mbox = recv)
 };
 
 using ptx::ld_acquire_sys;
@@ -168,7 +169,9 @@ __global__ void __launch_bounds__(1024) symm_coll_kernel(const SymmArgs a) {
   __syncthreads();
 
   const char* mine = a.mbox[a.me];
-  if (a.op == kCollAllGather) {
+  if (a.op == kCollAllGather && a.direct) {
+    // the peers wrote their slots of recv directly; the own slot was copied above
+  } else if (a.op == kCollAllGather) {
     for (int p = 0; p < a.P; ++p) {
       if (p == a.me) continue;
       const char* src = mine + p * a.slot_bytes;
@@ -313,6 +316,55 @@ void SymmHeap::arena_free(size_t off) {
       free_.erase(it);
     }
   }
+}
+
+void SymmHeap::all_gather_direct(const std::vector<int>& line, int pos, const void* send,
+                                 size_t recv_off, size_t count, int dtype, int num_sms,
+                                 cudaStream_t s) {
+  const int P = static_cast<int>(line.size());
+  if (P > kSymmMaxLine) fail(C3D_ERR_CONFIG_INVALID, "axis line longer than 8 ranks");
+  if (P == 1 || count == 0) return;
+  const size_t es = dtype_size(dtype);
+  SymmArgs a{};
+  a.op = kCollAllGather;
+  a.P = P;
+  a.me = pos;
+  a.rank = rank_;
+  a.direct = 1;
+  for (int p = 0; p < P; ++p) {
+    a.line[p] = line[p];
+    a.mbox[p] = arena_[line[p]] + recv_off;  // slot `me` of the peer's buffer: + me * count
+    a.entered[p] = entered_[line[p]];
+    a.done[p] = done_[line[p]];
+  }
+  a.my_entered = entered_[rank_];
+  a.my_done = done_[rank_];
+  a.my_seq = seq_;
+  a.send = static_cast<const char*>(send);
+  a.recv = arena_[rank_] + recv_off;
+  a.count = static_cast<long long>(count);
+  a.slot_bytes = static_cast<long long>(count * es);
+  a.c0 = 0;
+  a.n = static_cast<long long>(count);
+  static const size_t chunk = [] {
+    const char* e = std::getenv("C3D_SYMM_CHUNK_KB");
+    return static_cast<size_t>(e ? std::atoi(e) : 32) << 10;
+  }();
+  static const int per_sm = [] {
+    const char* e = std::getenv("C3D_SYMM_PER_SM");
+    return e ? std::atoi(e) : 2;
+  }();
+  const size_t blocks = (count * es + chunk - 1) / chunk;
+  a.G = static_cast<int>(std::max<size_t>(
+      1, std::min<size_t>(blocks, std::min(per_sm * num_sms, kSymmMaxBlocks))));
+  const bool vec_ok = reinterpret_cast<uintptr_t>(send) % 16 == 0 && recv_off % 16 == 0 &&
+                      count % (16 / es) == 0;
+  if (dtype == kF32) {
+    if (vec_ok) launch<kF32, true>(a, s); else launch<kF32, false>(a, s);
+  } else {
+    if (vec_ok) launch<kBF16, true>(a, s); else launch<kBF16, false>(a, s);
+  }
+  check_launch("symm_all_gather_direct");
 }
 
 void SymmHeap::collective(CollOp op, const std::vector<int>& line, int pos, const void* send,

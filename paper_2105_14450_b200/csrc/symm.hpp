@@ -49,6 +49,11 @@ class SymmHeap {
                   size_t count, int dtype, int root_pos, bool is_max, int num_sms,
                   cudaStream_t s);
 
+  // All-gather into a symmetric arena buffer (offset recv_off on every rank): each rank
+  // writes its shard straight into the peers' buffers -- no mailbox, no copy-out.
+  void all_gather_direct(const std::vector<int>& line, int pos, const void* send, size_t recv_off,
+                         size_t count, int dtype, int num_sms, cudaStream_t s);
+
   // Mailbox of rank `r` as mapped in this process (own heap for r == rank()).
   char* mailbox(int r) const { return mbox_[r]; }
   uint32_t* entered(int r) const { return entered_[r]; }
