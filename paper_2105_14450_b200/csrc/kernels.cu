@@ -291,6 +291,131 @@ __global__ void ln_bwd_dx_kernel(const void* dy, int dt, const void* xhat, int x
   }
 }
 
+// ---- vectorised LayerNorm: a warp per row, the row held in registers (8 values per
+// 16-B vector, VPL vectors per lane, cols = 256 * VPL); same arithmetic as above.
+__device__ __forceinline__ void vload8(const void* base, int dt, int64_t off, float (&v)[8]) {
+  if (dt == kBF16) {
+    const uint4 q = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      v[2 * i] = f.x;
+      v[2 * i + 1] = f.y;
+    }
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
+    const float4 b = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+__device__ __forceinline__ void vstore8(void* base, int dt, int64_t off, const float (&v)[8]) {
+  if (dt == kBF16) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off) = q;
+  } else {
+    *reinterpret_cast<float4*>(static_cast<float*>(base) + off) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(static_cast<float*>(base) + off + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+template <int VPL>
+__global__ void ln_fwd_vec_kernel(const void* x, int dt, int64_t rows, float eps,
+                                  const float* gamma, const float* beta, void* y, int ydt,
+                                  void* xhat, int xhdt, float* inv_std) {
+  constexpr int64_t cols = 256 * VPL;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float v[VPL][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    vload8(x, dt, r * cols + (k * 32 + lane) * 8, v[k]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[k][i];
+  }
+  const float inv_h = 1.f / static_cast<float>(cols);
+  const float mean = warp_sum(s) * inv_h;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float d = v[k][i] - mean;
+      q += d * d;
+    }
+  const float inv = 1.f / sqrtf(warp_sum(q) * inv_h + eps);
+  if (lane == 0 && inv_std) inv_std[r] = inv;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t c = (k * 32 + lane) * 8;
+    float xh[8], o[8];
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + c));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + c + 4));
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xh[i] = (v[k][i] - mean) * inv;
+      o[i] = g[i] * xh[i] + bb[i];
+    }
+    if (xhat) vstore8(xhat, xhdt, r * cols + c, xh);
+    vstore8(y, ydt, r * cols + c, o);
+  }
+}
+
+// Row statistics and dx in one pass when they need no all-reduce (p_out = 1):
+// g = dy * gamma, s = sum g, d = sum g * xhat, dx = inv_std * (g - s/h - xhat * d/h) (+ resid).
+template <int VPL>
+__global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int xdt,
+                                  const float* gamma, const float* inv_std, int64_t rows,
+                                  const void* resid, int rdt, void* dx, int dxdt) {
+  constexpr int64_t cols = 256 * VPL;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float g[VPL][8], xh[VPL][8];
+  float s = 0.f, d = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t c = (k * 32 + lane) * 8;
+    vload8(dy, dt, r * cols + c, g[k]);
+    vload8(xhat, xdt, r * cols + c, xh[k]);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+    const float gm[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      g[k][i] *= gm[i];
+      s += g[k][i];
+      d += g[k][i] * xh[k][i];
+    }
+  }
+  const float inv_h = 1.f / static_cast<float>(cols);
+  s = warp_sum(s) * inv_h;
+  d = warp_sum(d) * inv_h;
+  const float inv = inv_std[r];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t c = (k * 32 + lane) * 8;
+    float o[8], rr[8];
+    if (resid) vload8(resid, rdt, r * cols + c, rr);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i] = inv * (g[k][i] - s - xh[k][i] * d);
+      if (resid) o[i] += rr[i];
+    }
+    vstore8(dx, dxdt, r * cols + c, o);
+  }
+}
+
 __global__ void copy_heads_kernel(const void* src, int64_t src_ld, int64_t src_hs, void* dst,
                                   int64_t dst_ld, int64_t dst_hs, int64_t rows, int64_t heads,
                                   int64_t dh, int dt) {
@@ -391,13 +516,52 @@ void k_ln_apply(const void* x, int dt, int64_t rows, int64_t cols, const float* 
   check_launch("ln_apply");
 }
 
+namespace {
+bool al16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+int ln_vpl(int64_t cols) {
+  return (cols == 256 || cols == 512 || cols == 1024 || cols == 2048) ? static_cast<int>(cols / 256) : 0;
+}
+}  // namespace
+
 void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps,
                     const float* gamma, const float* beta, void* y, int ydt, void* xhat,
                     int xhdt, float* inv_std, cudaStream_t s) {
   if (rows == 0) return;
+  const int vpl = ln_vpl(cols);
+  if (vpl && al16(x) && al16(y) && (!xhat || al16(xhat)) && al16(gamma) && al16(beta)) {
+    auto launch = [&](auto kern) {
+      kern<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(x, dt, rows, eps, gamma, beta, y, ydt,
+                                                            xhat, xhdt, inv_std);
+    };
+    if (vpl == 1) launch(ln_fwd_vec_kernel<1>);
+    else if (vpl == 2) launch(ln_fwd_vec_kernel<2>);
+    else if (vpl == 4) launch(ln_fwd_vec_kernel<4>);
+    else launch(ln_fwd_vec_kernel<8>);
+    check_launch("ln_fwd_vec");
+    return;
+  }
   ln_fwd_fused_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
       x, dt, rows, cols, eps, gamma, beta, y, ydt, xhat, xhdt, inv_std);
   check_launch("ln_fwd_fused");
+}
+
+bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                    const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
+                    void* dx, int dxdt, cudaStream_t s) {
+  const int vpl = ln_vpl(cols);
+  if (!vpl || !al16(dy) || !al16(xhat) || !al16(gamma) || !al16(dx) || (resid && !al16(resid)))
+    return false;
+  if (rows == 0) return true;
+  auto launch = [&](auto kern) {
+    kern<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(dy, dt, xhat, xdt, gamma, inv_std, rows,
+                                                          resid, rdt, dx, dxdt);
+  };
+  if (vpl == 1) launch(ln_bwd_vec_kernel<1>);
+  else if (vpl == 2) launch(ln_bwd_vec_kernel<2>);
+  else if (vpl == 4) launch(ln_bwd_vec_kernel<4>);
+  else launch(ln_bwd_vec_kernel<8>);
+  check_launch("ln_bwd_vec");
+  return true;
 }
 
 void k_ln_bwd_rows(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,

@@ -44,6 +44,11 @@ void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps
                     const float* gamma, const float* beta, void* y, int ydt, void* xhat,
                     int xhdt, float* inv_std, cudaStream_t s);
 // row_sum[r] = sum_c dy*gamma, row_dot[r] = sum_c dy*gamma*xhat (into rs[0:rows], rs[rows:2rows]).
+// p_out = 1 backward in one pass (row sums and dx); false when the shape has no
+// vectorised form (the caller then runs k_ln_bwd_rows + k_ln_bwd_dx).
+bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                    const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
+                    void* dx, int dxdt, cudaStream_t s);
 void k_ln_bwd_rows(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
                    int64_t rows, int64_t cols, float* rs, cudaStream_t s);
 // dx = inv_std*(dy*gamma - row_sum*inv_h - xhat*row_dot*inv_h) (+ resid).

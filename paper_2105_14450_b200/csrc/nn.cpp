@@ -218,11 +218,15 @@ void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const 
     outs[0].len = outs[1].len = dy.hidden;
     reduce_to_diagonal(cube, d, cs.as<float>(), 2, outs, s);
   }
+  dx = make_act(cube, dx.data, dx.dtype, dy.batch, dy.seq, dy.hidden, dy.group);
+  if (cube.extent(d.out) == 1 &&
+      k_ln_bwd_fused(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, sv.inv_std, dy.rows,
+                     dy.cols, resid, dx.dtype, dx.data, dx.dtype, s))
+    return;
   DevBuf rs(static_cast<size_t>(2 * dy.rows) * sizeof(float), s);
   k_ln_bwd_rows(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, dy.rows, dy.cols,
                 rs.as<float>(), s);
   cube.all_reduce(d.out, rs.get(), 2 * dy.rows, kF32, false, s);
-  dx = make_act(cube, dx.data, dx.dtype, dy.batch, dy.seq, dy.hidden, dy.group);
   k_ln_bwd_dx(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, sv.inv_std, rs.as<float>(),
               inv_h, dy.rows, dy.cols, resid, dx.dtype, dx.data, dx.dtype, s);
 }
