@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.hpp"
 #include "epi.cuh"
@@ -326,7 +327,8 @@ __device__ __forceinline__ void vstore8(void* base, int dt, int64_t off, const f
 template <int VPL>
 __global__ void ln_fwd_vec_kernel(const void* x, int dt, int64_t rows, float eps,
                                   const float* gamma, const float* beta, void* y, int ydt,
-                                  void* xhat, int xhdt, float* inv_std) {
+                                  void* xhat, int xhdt, float* inv_std, const float* gsums,
+                                  const float* gsq, float ginv_h) {
   constexpr int64_t cols = 256 * VPL;
   const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -339,17 +341,23 @@ __global__ void ln_fwd_vec_kernel(const void* x, int dt, int64_t rows, float eps
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += v[k][i];
   }
-  const float inv_h = 1.f / static_cast<float>(cols);
-  const float mean = warp_sum(s) * inv_h;
-  float q = 0.f;
+  float mean, inv;
+  if (gsums) {  // statistics all-reduced along the output axis
+    mean = gsums[r] * ginv_h;
+    inv = 1.f / sqrtf(gsq[r] * ginv_h + eps);
+  } else {
+    const float inv_h = 1.f / static_cast<float>(cols);
+    mean = warp_sum(s) * inv_h;
+    float q = 0.f;
 #pragma unroll
-  for (int k = 0; k < VPL; ++k)
+    for (int k = 0; k < VPL; ++k)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float d = v[k][i] - mean;
-      q += d * d;
-    }
-  const float inv = 1.f / sqrtf(warp_sum(q) * inv_h + eps);
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[k][i] - mean;
+        q += d * d;
+      }
+    inv = 1.f / sqrtf(warp_sum(q) * inv_h + eps);
+  }
   if (lane == 0 && inv_std) inv_std[r] = inv;
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -371,12 +379,71 @@ __global__ void ln_fwd_vec_kernel(const void* x, int dt, int64_t rows, float eps
   }
 }
 
+// Row sum (sums == null) or centred sum of squares of a row held in registers.
+template <int VPL>
+__global__ void row_sum_vec_kernel(const void* x, int dt, int64_t rows, const float* sums,
+                                   float inv_h, float* out) {
+  constexpr int64_t cols = 256 * VPL;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  const float mean = sums ? sums[r] * inv_h : 0.f;
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    float v[8];
+    vload8(x, dt, r * cols + (k * 32 + lane) * 8, v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (sums) {
+        const float d = v[i] - mean;
+        acc += d * d;
+      } else {
+        acc += v[i];
+      }
+    }
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[r] = acc;
+}
+
+template <int VPL>
+__global__ void ln_bwd_rows_vec_kernel(const void* dy, int dt, const void* xhat, int xdt,
+                                       const float* gamma, int64_t rows, float* rs) {
+  constexpr int64_t cols = 256 * VPL;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float s = 0.f, d = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int64_t c = (k * 32 + lane) * 8;
+    float g[8], xh[8];
+    vload8(dy, dt, r * cols + c, g);
+    vload8(xhat, xdt, r * cols + c, xh);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float gg = g[i] * __ldg(gamma + c + i);
+      s += gg;
+      d += gg * xh[i];
+    }
+  }
+  s = warp_sum(s);
+  d = warp_sum(d);
+  if (lane == 0) {
+    rs[r] = s;
+    rs[rows + r] = d;
+  }
+}
+
 // Row statistics and dx in one pass when they need no all-reduce (p_out = 1):
 // g = dy * gamma, s = sum g, d = sum g * xhat, dx = inv_std * (g - s/h - xhat * d/h) (+ resid).
+// With `grs` the row sums come all-reduced ([s | d], scaled by ginv_h).
 template <int VPL>
 __global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int xdt,
                                   const float* gamma, const float* inv_std, int64_t rows,
-                                  const void* resid, int rdt, void* dx, int dxdt) {
+                                  const void* resid, int rdt, void* dx, int dxdt,
+                                  const float* grs, float ginv_h) {
   constexpr int64_t cols = 256 * VPL;
   const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -398,9 +465,14 @@ __global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int 
       d += g[k][i] * xh[k][i];
     }
   }
-  const float inv_h = 1.f / static_cast<float>(cols);
-  s = warp_sum(s) * inv_h;
-  d = warp_sum(d) * inv_h;
+  if (grs) {
+    s = grs[r] * ginv_h;
+    d = grs[rows + r] * ginv_h;
+  } else {
+    const float inv_h = 1.f / static_cast<float>(cols);
+    s = warp_sum(s) * inv_h;
+    d = warp_sum(d) * inv_h;
+  }
   const float inv = inv_std[r];
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
@@ -499,9 +571,31 @@ void k_mul_cols(const void* a, int adt, const float* b, void* c, int cdt, int64_
   check_launch("mul_cols");
 }
 
+namespace {
+bool al16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
+int ln_vpl(int64_t cols) {
+  return (cols == 256 || cols == 512 || cols == 1024 || cols == 2048) ? static_cast<int>(cols / 256) : 0;
+}
+template <typename F>
+void by_vpl(int vpl, F&& f) {
+  if (vpl == 1) f(std::integral_constant<int, 1>{});
+  else if (vpl == 2) f(std::integral_constant<int, 2>{});
+  else if (vpl == 4) f(std::integral_constant<int, 4>{});
+  else f(std::integral_constant<int, 8>{});
+}
+}  // namespace
+
 void k_row_sum(const void* x, int dt, int64_t rows, int64_t cols, const float* sums,
                float inv_h, float* out, cudaStream_t s) {
   if (rows == 0) return;
+  if (const int vpl = ln_vpl(cols); vpl && al16(x)) {
+    by_vpl(vpl, [&](auto V) {
+      row_sum_vec_kernel<decltype(V)::value><<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
+          x, dt, rows, sums, inv_h, out);
+    });
+    check_launch("row_sum_vec");
+    return;
+  }
   row_sum_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(x, dt, rows, cols, sums, inv_h,
                                                                   out);
   check_launch("row_sum");
@@ -511,17 +605,19 @@ void k_ln_apply(const void* x, int dt, int64_t rows, int64_t cols, const float* 
                 const float* sq, float inv_h, float eps, const float* gamma, const float* beta,
                 void* y, int ydt, void* xhat, int xhdt, float* inv_std, cudaStream_t s) {
   if (rows == 0) return;
+  if (const int vpl = ln_vpl(cols);
+      vpl && al16(x) && al16(y) && (!xhat || al16(xhat)) && al16(gamma) && al16(beta)) {
+    by_vpl(vpl, [&](auto V) {
+      ln_fwd_vec_kernel<decltype(V)::value><<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
+          x, dt, rows, eps, gamma, beta, y, ydt, xhat, xhdt, inv_std, sums, sq, inv_h);
+    });
+    check_launch("ln_apply_vec");
+    return;
+  }
   ln_apply_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
       x, dt, rows, cols, sums, sq, inv_h, eps, gamma, beta, y, ydt, xhat, xhdt, inv_std);
   check_launch("ln_apply");
 }
-
-namespace {
-bool al16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
-int ln_vpl(int64_t cols) {
-  return (cols == 256 || cols == 512 || cols == 1024 || cols == 2048) ? static_cast<int>(cols / 256) : 0;
-}
-}  // namespace
 
 void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps,
                     const float* gamma, const float* beta, void* y, int ydt, void* xhat,
@@ -531,7 +627,8 @@ void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps
   if (vpl && al16(x) && al16(y) && (!xhat || al16(xhat)) && al16(gamma) && al16(beta)) {
     auto launch = [&](auto kern) {
       kern<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(x, dt, rows, eps, gamma, beta, y, ydt,
-                                                            xhat, xhdt, inv_std);
+                                                            xhat, xhdt, inv_std, nullptr, nullptr,
+                                                            0.f);
     };
     if (vpl == 1) launch(ln_fwd_vec_kernel<1>);
     else if (vpl == 2) launch(ln_fwd_vec_kernel<2>);
@@ -554,7 +651,7 @@ bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const flo
   if (rows == 0) return true;
   auto launch = [&](auto kern) {
     kern<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(dy, dt, xhat, xdt, gamma, inv_std, rows,
-                                                          resid, rdt, dx, dxdt);
+                                                          resid, rdt, dx, dxdt, nullptr, 0.f);
   };
   if (vpl == 1) launch(ln_bwd_vec_kernel<1>);
   else if (vpl == 2) launch(ln_bwd_vec_kernel<2>);
@@ -567,6 +664,14 @@ bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const flo
 void k_ln_bwd_rows(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
                    int64_t rows, int64_t cols, float* rs, cudaStream_t s) {
   if (rows == 0) return;
+  if (const int vpl = ln_vpl(cols); vpl && al16(dy) && al16(xhat)) {
+    by_vpl(vpl, [&](auto V) {
+      ln_bwd_rows_vec_kernel<decltype(V)::value><<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
+          dy, dt, xhat, xdt, gamma, rows, rs);
+    });
+    check_launch("ln_bwd_rows_vec");
+    return;
+  }
   ln_bwd_rows_kernel<<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(dy, dt, xhat, xdt, gamma,
                                                                       rows, cols, rs);
   check_launch("ln_bwd_rows");
@@ -576,6 +681,15 @@ void k_ln_bwd_dx(const void* dy, int dt, const void* xhat, int xdt, const float*
                  const float* inv_std, const float* rs, float inv_h, int64_t rows, int64_t cols,
                  const void* resid, int rdt, void* dx, int dxdt, cudaStream_t s) {
   if (rows * cols == 0) return;
+  if (const int vpl = ln_vpl(cols);
+      vpl && al16(dy) && al16(xhat) && al16(gamma) && al16(dx) && (!resid || al16(resid))) {
+    by_vpl(vpl, [&](auto V) {
+      ln_bwd_vec_kernel<decltype(V)::value><<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
+          dy, dt, xhat, xdt, gamma, inv_std, rows, resid, rdt, dx, dxdt, rs, inv_h);
+    });
+    check_launch("ln_bwd_dx_vec");
+    return;
+  }
   ln_bwd_dx_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dy, dt, xhat, xdt, gamma, inv_std, rs,
                                                          inv_h, rows, cols, resid, rdt, dx, dxdt);
   check_launch("ln_bwd_dx");

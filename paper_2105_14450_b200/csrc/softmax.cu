@@ -150,10 +150,46 @@ void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int
                       const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s) {
   LAUNCH_ROWS(bwd_ds_kernel, "softmax_bwd_ds", dp, p, pdt, rows, cols, rowdot, scale, ds, dsdt);
 }
+// dh = 64, bf16: 8 threads per row, one 16-B vector of each operand per thread.
+__global__ void attn_rowdot64_kernel(const __nv_bfloat16* d_o, const __nv_bfloat16* o,
+                                     int64_t rows, int64_t S, int64_t H, int64_t sb_hi,
+                                     float* out) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t r = t / 8;
+  const int part = static_cast<int>(t % 8);
+  float acc = 0.f;
+  if (r < rows) {
+    const int64_t b = r / S, q = r - (r / S) * S;
+    const int64_t base = (b / H) * sb_hi + q * (H * 64) + (b % H) * 64 + part * 8;
+    const uint4 x = *reinterpret_cast<const uint4*>(d_o + base);
+    const uint4 y = *reinterpret_cast<const uint4*>(o + base);
+    const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 a = __bfloat1622float2(hx[i]);
+      const float2 c = __bfloat1622float2(hy[i]);
+      acc += a.x * c.x + a.y * c.y;
+    }
+  }
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (r < rows && part == 0) out[r] = acc;
+}
+
 void k_attn_rowdot(const void* d_o, const void* o, int dt, int64_t nslices, int64_t S, int64_t H,
                    int64_t dh, int64_t sb_hi, float* out, cudaStream_t s) {
   const int64_t rows = nslices * S;
   if (rows == 0) return;
+  if (dt == kBF16 && dh == 64 && reinterpret_cast<uintptr_t>(d_o) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(o) % 16 == 0 && sb_hi % 8 == 0) {
+    const int64_t threads = rows * 8;
+    attn_rowdot64_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(d_o), static_cast<const __nv_bfloat16*>(o), rows, S, H,
+        sb_hi, out);
+    check_launch("attn_rowdot64");
+    return;
+  }
   attn_rowdot_kernel<<<blocks_for(rows), kWarps * 32, 0, s>>>(d_o, o, dt, rows, S, H, dh, sb_hi, out);
   check_launch("attn_rowdot");
 }
