@@ -31,7 +31,8 @@ namespace {
 
 constexpr int kQ = 128;   // queries per CTA (UMMA M)
 constexpr int kDh = 64;   // head dim (one 128-B K block)
-constexpr int kThreadsAttn = 192;  // warp 0 TMA, warp 1 MMA, warps 2..5 softmax rows
+constexpr int kSoftWarps = 16;     // 4 TMEM lane quarters x 4 column groups
+constexpr int kThreadsAttn = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 MMA, softmax warps
 
 struct AttnArgs {
   int S, keys, H;
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
   uint64_t* bar_p = bars + 3;
   uint64_t* bar_o = bars + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  float* red = reinterpret_cast<float*>(bars + 8);  // [2][4 groups][128 rows] row partials
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int q0 = blockIdx.x * kQ;
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
     ptx::mbar_init(bar_qk, 1);
     ptx::mbar_init(bar_v, 1);
     ptx::mbar_init(bar_s, 1);
-    ptx::mbar_init(bar_p, 128);
+    ptx::mbar_init(bar_p, 32 * kSoftWarps);
     ptx::mbar_init(bar_o, 1);
     ptx::fence_barrier_init();
   }
@@ -132,35 +134,45 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
       ptx::umma_commit(bar_o);
     }
   } else {
-    // ---------------- softmax rows: warp w owns TMEM lanes 32*(w % 4) .. +32
+    // ---------------- softmax: warp w owns TMEM lanes 32*(w % 4) .. +32 and column group
+    // (w - 2) / 4 (a quarter of the keys); row max / sum combine through shared memory
+    constexpr int kGroupCols = KEYS / 4;
     const int quarter = warp & 3;
+    const int group = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const int c0 = group * kGroupCols;
     ptx::mbar_wait(bar_s, 0);
     ptx::tc_fence_after();
     float m = -INFINITY;
 #pragma unroll 1
-    for (int c = 0; c < KEYS / 32; ++c) {
+    for (int c = c0; c < c0 + kGroupCols; c += 32) {
       float v[32];
-      ptx::tmem_ld32(trow + c * 32, v);
+      ptx::tmem_ld32(trow + c, v);
 #pragma unroll
       for (int j = 0; j < 32; ++j) m = fmaxf(m, v[j]);
     }
+    red[group * kQ + row] = m;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
+    m = fmaxf(fmaxf(red[row], red[kQ + row]), fmaxf(red[2 * kQ + row], red[3 * kQ + row]));
     const float ms = m * args.scale_log2;
     float sum = 0.f;
 #pragma unroll 1
-    for (int c = 0; c < KEYS / 32; ++c) {
+    for (int c = c0; c < c0 + kGroupCols; c += 32) {
       float v[32];
-      ptx::tmem_ld32(trow + c * 32, v);
+      ptx::tmem_ld32(trow + c, v);
 #pragma unroll
       for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(v[j], args.scale_log2, -ms));
     }
+    red[4 * kQ + group * kQ + row] = sum;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
+    sum = (red[4 * kQ + row] + red[5 * kQ + row]) + (red[6 * kQ + row] + red[7 * kQ + row]);
     const float inv = 1.f / sum;
 #pragma unroll 1
-    for (int c = 0; c < KEYS / 32; ++c) {
+    for (int c = c0; c < c0 + kGroupCols; c += 32) {
       float v[32];
-      ptx::tmem_ld32(trow + c * 32, v);
-      uint8_t* chunk_row = sP + (c >> 1) * 16384 + row * 128;
+      ptx::tmem_ld32(trow + c, v);
+      uint8_t* chunk_row = sP + (c >> 6) * 16384 + row * 128;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 pk;
@@ -172,7 +184,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
                          exp2f(fmaf(v[8 * j + 5], args.scale_log2, -ms)) * inv);
         pk.w = pack_bf16(exp2f(fmaf(v[8 * j + 6], args.scale_log2, -ms)) * inv,
                          exp2f(fmaf(v[8 * j + 7], args.scale_log2, -ms)) * inv);
-        const int chunk = (c & 1) * 4 + j;
+        const int chunk = ((c >> 5) & 1) * 4 + j;
         *reinterpret_cast<uint4*>(chunk_row + ((chunk ^ (row & 7)) << 4)) = pk;
       }
     }
@@ -181,29 +193,30 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
     ptx::tc_fence_before();
     ptx::mbar_arrive(bar_p);
     // probabilities to global (saved for the backward): one TMA store per 64-key chunk
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
     if (warp == 2 && lane == 0) {
 #pragma unroll
       for (int kb = 0; kb < KEYS / 64; ++kb)
         ptx::tma_store_5d(&tmP, sP + kb * 16384, kb * 64, q0, 0, c3, c4);
       ptx::bulk_commit();
     }
-    // context row: O (fp32 in TMEM columns 0..63) -> bf16
-    ptx::mbar_wait(bar_o, 0);
-    ptx::tc_fence_after();
-    float o[64];
-    ptx::tmem_ld32(trow, *reinterpret_cast<float(*)[32]>(o));
-    ptx::tmem_ld32(trow + 32, *reinterpret_cast<float(*)[32]>(o + 32));
-    __nv_bfloat16* dst = args.ctx + c3 * args.ctx_sb_lo + c4 * args.ctx_sb_hi +
-                         static_cast<long long>(q0 + row) * args.ctx_sr;
+    // context row: O (fp32 in TMEM columns 0..63) -> bf16, 32 columns per group 0 / 1
+    if (group < 2) {
+      ptx::mbar_wait(bar_o, 0);
+      ptx::tc_fence_after();
+      float o[32];
+      ptx::tmem_ld32(trow + group * 32, o);
+      __nv_bfloat16* dst = args.ctx + c3 * args.ctx_sb_lo + c4 * args.ctx_sb_hi +
+                           static_cast<long long>(q0 + row) * args.ctx_sr + group * 32;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint4 pk;
-      pk.x = pack_bf16(o[8 * j + 0], o[8 * j + 1]);
-      pk.y = pack_bf16(o[8 * j + 2], o[8 * j + 3]);
-      pk.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
-      pk.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
-      reinterpret_cast<uint4*>(dst)[j] = pk;
+      for (int j = 0; j < 4; ++j) {
+        uint4 pk;
+        pk.x = pack_bf16(o[8 * j + 0], o[8 * j + 1]);
+        pk.y = pack_bf16(o[8 * j + 2], o[8 * j + 3]);
+        pk.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
+        pk.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
+        reinterpret_cast<uint4*>(dst)[j] = pk;
+      }
     }
     if (warp == 2 && lane == 0) ptx::bulk_wait_all();
   }
@@ -221,7 +234,7 @@ void launch_attn(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& 
   constexpr int kQBytes = kQ * kDh * 2, kKBytes = KEYS * kDh * 2;
   constexpr int kPBytes = KEYS / 64 * kQ * 128;
   constexpr int kVOff = (kQBytes + kKBytes > kPBytes ? kQBytes + kKBytes : kPBytes);
-  constexpr int smem = 1024 + kVOff + KEYS * kDh * 2 + 64;
+  constexpr int smem = 1024 + kVOff + KEYS * kDh * 2 + 64 + 8 * kQ * 4;
   auto kern = attn_fwd_kernel<KEYS>;
   static bool attr = false;
   if (!attr) {
