@@ -279,6 +279,18 @@ int c3d_linear_bwd(c3d_cube* cube, int mode, const c3d_activation* dy, const c3d
                    const c3d_linear_params* p, c3d_activation* dx, c3d_matrix* dweight,
                    c3d_vector* dbias, void* stream);
 
+/* 3-D cross-entropy (not in the reference): logits = x W + b
+ * through the 3-D linear (fp32 logits), loss = mean over the batch*seq tokens of
+ * logsumexp(logits) - logits[target]. `targets`: int32 device array of the GLOBAL
+ * token targets [batch * seq] (identical on every rank; must stay valid until
+ * c3d_loss_bwd). `loss`: one device float, identical on every rank. The backward
+ * returns dx, dW, db of the head in `grad_dtype` for dx (dW / db in their
+ * descriptors' dtypes). */
+int c3d_loss_fwd(c3d_cube* cube, int mode, const c3d_activation* x, const c3d_linear_params* head,
+                 const int32_t* targets, int* group, float* loss, c3d_saved** saved, void* stream);
+int c3d_loss_bwd(c3d_cube* cube, int mode, const c3d_saved* saved, const c3d_linear_params* head,
+                 c3d_activation* dx, c3d_matrix* dweight, c3d_vector* dbias, void* stream);
+
 /* LayerNormParams (cube3d/nn.hpp:119-124); layernorm3d_fwd/bwd (:140-222). */
 typedef struct {
   c3d_vector gamma, beta;

@@ -270,6 +270,32 @@ def layernorm_bwd(dy, cache):
     return dx, dgamma, dbeta
 
 
+def cross_entropy_fwd(x, w, b, targets):
+    """The loss row X1 of SURVEY.md §8(a) -- NOT IN THE REFERENCE (its only loss is
+    <dY, Y>, cube3d/verify.hpp:611-617), so parity is unpinned by reference outputs: the
+    linear is the reference's ref_linear_fwd (cube3d/reference.hpp:65-73), the
+    log-softmax the max-shifted stable form, and tests/test_oracle_golden.py checks the
+    gradients against central finite differences (the reference's finite_diff,
+    cube3d/reference.hpp:389-405). -> (mean loss, cache)."""
+    logits = x @ w + b
+    m = logits.max(axis=1, keepdims=True)
+    e = np.exp(logits - m)
+    se = e.sum(axis=1, keepdims=True)
+    n = x.shape[0]
+    loss = float(np.mean(np.log(se[:, 0]) + m[:, 0] - logits[np.arange(n), targets]))
+    return loss, (x, w, e / se, targets)
+
+
+def cross_entropy_bwd(cache):
+    """-> (dx, dw, db) of the mean loss."""
+    x, w, p, targets = cache
+    n = x.shape[0]
+    dl = p.copy()
+    dl[np.arange(n), targets] -= 1.0
+    dl /= n
+    return dl @ w.T, x.T @ dl, dl.sum(axis=0)
+
+
 @dataclass
 class LayerParams:
     """GlobalLayerParams (transformer.hpp:182-194), float64."""

@@ -130,6 +130,10 @@ SIGNATURES = {
                        P(c3d_activation), P(VP), VP],
     "c3d_linear_bwd": [VP, C.c_int, P(c3d_activation), VP, P(c3d_linear_params),
                        P(c3d_activation), P(c3d_matrix), P(c3d_vector), VP],
+    "c3d_loss_fwd": [VP, C.c_int, P(c3d_activation), P(c3d_linear_params), VP, P(C.c_int), VP,
+                     P(VP), VP],
+    "c3d_loss_bwd": [VP, C.c_int, VP, P(c3d_linear_params), P(c3d_activation), P(c3d_matrix),
+                     P(c3d_vector), VP],
     "c3d_layernorm_fwd": [VP, P(c3d_activation), P(c3d_layernorm_params), P(c3d_activation),
                           P(VP), VP],
     "c3d_layernorm_bwd": [VP, P(c3d_activation), VP, P(c3d_activation), P(c3d_vector),

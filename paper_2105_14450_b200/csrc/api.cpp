@@ -28,7 +28,7 @@ struct c3d_rng {
 
 struct c3d_saved {
   std::unique_ptr<c3d::Saved> impl;
-  int kind = 0;  // 1 linear, 2 layernorm, 3 attention, 4 mlp, 5 layer
+  int kind = 0;  // 1 linear, 2 layernorm, 3 attention, 4 mlp, 5 layer, 6 loss
   int mode = 0;
 };
 
@@ -562,6 +562,53 @@ int c3d_linear_bwd(c3d_cube* cube, int mode, const c3d_activation* dy, const c3d
     if (dbias) db = vec_of(*dbias);
     c3d::linear_bwd(cb, mode, dya, sv, lp, dx ? &dxa : nullptr, dweight ? &dw : nullptr,
                     dbias ? &db : nullptr, nullptr, as_stream(stream));
+    if (dx) act_out(dxa, dx);
+    if (dweight && dw.data) c3d::to_c(dw, dweight);
+    if (dbias) dbias->global_len = lp.w.gcols;
+  });
+}
+
+int c3d_loss_fwd(c3d_cube* cube, int mode, const c3d_activation* x, const c3d_linear_params* head,
+                 const int32_t* targets, int* group, float* loss, c3d_saved** saved, void* stream) {
+  return guard([&] {
+    need(x, "x");
+    need(head, "head");
+    need(group, "group");
+    need(saved, "saved");
+    if (!targets || !loss) c3d::fail(C3D_ERR_CONFIG_INVALID, "loss needs targets and output");
+    auto& cb = get(cube);
+    c3d::Act xa = act_of(cb, *x);
+    c3d::LinearP lp;
+    lp.w = c3d::from_c(cb, head->weight);
+    lp.b = vec_of(head->bias);
+    lp.input_group = head->input_group;
+    auto sv = std::make_unique<c3d::LossSaved>();
+    c3d::loss_fwd(cb, mode, xa, lp, targets, *group, loss, sv.get(), as_stream(stream));
+    auto h = std::make_unique<c3d_saved>();
+    h->kind = 6;
+    h->impl = std::move(sv);
+    *saved = h.release();
+  });
+}
+int c3d_loss_bwd(c3d_cube* cube, int mode, const c3d_saved* saved, const c3d_linear_params* head,
+                 c3d_activation* dx, c3d_matrix* dweight, c3d_vector* dbias, void* stream) {
+  return guard([&] {
+    need(head, "head");
+    auto& cb = get(cube);
+    auto& sv = saved_as<c3d::LossSaved>(saved, 6);
+    c3d::LinearP lp;
+    lp.w = c3d::from_c(cb, head->weight);
+    lp.b = vec_of(head->bias);
+    lp.input_group = head->input_group;
+    c3d::Act dxa;
+    if (dx) dxa = act_dest(dx);
+    c3d::Mat dw;
+    if (dweight) dw = mat_dest(*dweight);
+    c3d::Vec db;
+    if (dbias) db = vec_of(*dbias);
+    const int gdt = dx ? dx->dtype : sv.lin.x.dtype;
+    c3d::loss_bwd(cb, mode, sv, lp, dx ? &dxa : nullptr, dweight ? &dw : nullptr,
+                  dbias ? &db : nullptr, gdt, as_stream(stream));
     if (dx) act_out(dxa, dx);
     if (dweight && dw.data) c3d::to_c(dw, dweight);
     if (dbias) dbias->global_len = lp.w.gcols;

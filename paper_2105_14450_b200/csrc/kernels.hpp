@@ -70,6 +70,21 @@ void k_softmax_bwd_rowdot(const float* dp, const void* p, int pdt, int64_t rows,
                           float* rowdot, cudaStream_t s);
 void k_softmax_bwd_ds(const float* dp, const void* p, int pdt, int64_t rows, int64_t cols,
                       const float* rowdot, float scale, void* ds, int dsdt, cudaStream_t s);
+// ---- cross-entropy (loss.cu): local logits row -> global token and vocabulary offset
+struct LossMap {
+  int64_t w = 0, a = 0;      // coordinates on x and on the logits' input axis
+  int64_t bl = 0, sl = 0;    // local batch and sequence extents
+  int64_t seq = 0;           // global sequence length
+  int64_t col0 = 0;          // first vocabulary column of the local block
+};
+void k_loss_stats(const float* logits, int64_t rows, int64_t cols, const float* mx,
+                  const int32_t* targets, const LossMap& map, float* st, cudaStream_t s);
+void k_loss_reduce(const float* mx, const float* st, int64_t rows, float scale, float* out,
+                   cudaStream_t s);
+void k_loss_grad(const float* logits, int64_t rows, int64_t cols, const float* mx, const float* st,
+                 const int32_t* targets, const LossMap& map, float scale, void* out, int dt,
+                 cudaStream_t s);
+
 // Row dot products sum_d dO*O of packed [bi][q][head][dh] buffers (softmax backward).
 void k_attn_rowdot(const void* d_o, const void* o, int dt, int64_t nslices, int64_t S, int64_t H,
                    int64_t dh, int64_t sb_hi, float* out, cudaStream_t s);

@@ -718,3 +718,66 @@ void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const Lay
 }
 
 }  // namespace c3d
+
+namespace c3d {
+
+// ------------------------------------------------------------------- loss
+
+void loss_fwd(Cube& cube, int mode, const Act& x, const LinearP& head, const int32_t* targets,
+              int& group, float* loss, LossSaved* sv, cudaStream_t s) {
+  if (!targets || !loss || !sv) fail(C3D_ERR_CONFIG_INVALID, "loss needs targets, output, saved");
+  const int g_out = 1 - x.group;
+  const ActGeom lg = act_geom(cube.grid(), x.batch, x.seq, head.w.gcols, g_out);
+  DevBuf& lb = sv->keep(DevBuf(static_cast<size_t>(lg.bl * lg.sl * lg.hl) * sizeof(float), s));
+  Act logits;
+  logits.data = lb.get();
+  logits.dtype = kF32;
+  linear_fwd(cube, mode, x, head, group, logits, &sv->lin, true, LinearEpi{}, s);
+  sv->logits = logits;
+  const int64_t rows = logits.rows, cols = logits.cols;
+  const int col_axis = lg.out_axis;
+  sv->mx = sv->keep(DevBuf(static_cast<size_t>(rows) * sizeof(float), s)).as<float>();
+  sv->st = sv->keep(DevBuf(static_cast<size_t>(2 * rows) * sizeof(float), s)).as<float>();
+  k_softmax_rowmax(static_cast<const float*>(logits.data), rows, cols, sv->mx, s);
+  cube.all_reduce(col_axis, sv->mx, rows, kF32, true, s);
+  LossMap map;
+  map.w = cube.coord(kX);
+  map.a = cube.coord(lg.in_axis);
+  map.bl = lg.bl;
+  map.sl = lg.sl;
+  map.seq = x.seq;
+  map.col0 = static_cast<int64_t>(cube.coord(col_axis)) * cols;
+  k_loss_stats(static_cast<const float*>(logits.data), rows, cols, sv->mx, targets, map, sv->st, s);
+  cube.all_reduce(col_axis, sv->st, 2 * rows, kF32, false, s);
+  sv->targets = targets;
+  sv->col0 = map.col0;
+  sv->tokens = x.batch * x.seq;
+  sv->map_w = map.w;
+  sv->map_a = map.a;
+  k_loss_reduce(sv->mx, sv->st, rows, 1.f / static_cast<float>(sv->tokens), loss, s);
+  // every token row sits on one rank of each (x, input-axis) line
+  cube.all_reduce(kX, loss, 1, kF32, false, s);
+  cube.all_reduce(lg.in_axis, loss, 1, kF32, false, s);
+}
+
+void loss_bwd(Cube& cube, int mode, const LossSaved& sv, const LinearP& head, Act* dx, Mat* dw,
+              const Vec* db, int grad_dtype, cudaStream_t s) {
+  const Act& lg = sv.logits;
+  DevBuf gb(lg.elems() * dtype_size(grad_dtype), s);
+  Act dl = lg;
+  dl.data = gb.get();
+  dl.dtype = grad_dtype;
+  const ActGeom geo = act_geom(cube.grid(), lg.batch, lg.seq, lg.hidden, lg.group);
+  LossMap map;
+  map.w = sv.map_w;
+  map.a = sv.map_a;
+  map.bl = geo.bl;
+  map.sl = geo.sl;
+  map.seq = lg.seq;
+  map.col0 = sv.col0;
+  k_loss_grad(static_cast<const float*>(lg.data), lg.rows, lg.cols, sv.mx, sv.st, sv.targets, map,
+              1.f / static_cast<float>(sv.tokens), dl.data, grad_dtype, s);
+  linear_bwd(cube, mode, dl, sv.lin, head, dx, dw, db, nullptr, s);
+}
+
+}  // namespace c3d

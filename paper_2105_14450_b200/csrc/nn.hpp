@@ -91,6 +91,17 @@ struct LayerSaved : Saved {
   Operand wg[4];  // qkv, out, fc1, fc2
 };
 
+// 3-D cross-entropy (loss.cu): logits kept in fp32 with their row statistics.
+struct LossSaved : Saved {
+  LinearSaved lin;
+  Act logits;  // fp32
+  float* mx = nullptr;
+  float* st = nullptr;  // [sum exp | target logit], all-reduced along the vocabulary axis
+  const int32_t* targets = nullptr;
+  int64_t col0 = 0, tokens = 0;
+  int64_t map_w = 0, map_a = 0;
+};
+
 struct LayerP {
   Vec ln1_g, ln1_b;
   LinearP qkv, out;
@@ -145,6 +156,14 @@ void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSa
              const LinearP& fc1, const LinearP& fc2, Act& dx, LayerG& g, cudaStream_t s,
              const Operand* fc1_wg = nullptr, const Operand* fc2_wg = nullptr,
              const LinearSinks* fc1_sinks = nullptr, const LinearSinks* fc2_sinks = nullptr);
+
+// Mean cross-entropy of softmax(x W + b) against global token targets (int32 [batch *
+// seq], device); `loss` is one device float (identical on every rank). `targets` must
+// stay valid until loss_bwd.
+void loss_fwd(Cube& cube, int mode, const Act& x, const LinearP& head, const int32_t* targets,
+              int& group, float* loss, LossSaved* saved, cudaStream_t s);
+void loss_bwd(Cube& cube, int mode, const LossSaved& sv, const LinearP& head, Act* dx, Mat* dw,
+              const Vec* db, int grad_dtype, cudaStream_t s);
 
 void layer_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LayerP& p, int& group,
                Act& y, LayerSaved* saved, cudaStream_t s);

@@ -830,6 +830,40 @@ def linear3d_bwd(cube, dy: Activation3D, saved: Saved, params: LinearParams, mod
     return dx, dw, db
 
 
+def cross_entropy_fwd(cube, x: Activation3D, head: LinearParams, targets, gs: GroupState,
+                      mode=MODE_AUTO, stream=None):
+    """3-D cross-entropy: mean over the batch*seq tokens of
+    logsumexp(x W + b) - (x W + b)[target]. `targets`: global int32 device tensor
+    [batch * seq] (kept alive by the returned state). -> (loss device scalar, saved)."""
+    torch = _torch()
+    t = targets.to(device=x.local.device, dtype=torch.int32).contiguous()
+    loss = torch.zeros(1, dtype=torch.float32, device=x.local.device)
+    cx, cp = x.c(), head.c()
+    g = C.c_int(gs.input_group)
+    h = C.c_void_p()
+    call("c3d_loss_fwd", cube.handle, mode, C.byref(cx), C.byref(cp), C.c_void_p(t.data_ptr()),
+         C.byref(g), C.c_void_p(loss.data_ptr()), C.byref(h), _stream(stream))
+    gs.input_group = g.value
+    sv = Saved(h)
+    sv.keep = (t, x.batch, x.seq, x.hidden, x.group, c3d_dtype(x.local))
+    return loss, sv
+
+
+def cross_entropy_bwd(cube, saved: Saved, head: LinearParams, mode=MODE_AUTO, stream=None,
+                      db_dtype=F32):
+    """-> (dx, dweight, dbias) of cross_entropy_fwd."""
+    _, batch, seq, hidden, group, dt = saved.keep
+    w = head.weight
+    dx = _act_out(cube, batch, seq, hidden, group, dt)
+    torch = _torch()
+    dw = ShardedMatrix(torch.empty_like(w.shard), w.global_rows, w.global_cols, w.layout, w.dirs)
+    db = _vec_out(cube, w.global_cols, db_dtype)
+    cp, cdx, cdw, cdb = head.c(), dx.c(), dw.c(), db.c()
+    call("c3d_loss_bwd", cube.handle, mode, saved._h, C.byref(cp), C.byref(cdx), C.byref(cdw),
+         C.byref(cdb), _stream(stream))
+    return dx, dw, db
+
+
 @dataclass
 class LayerNormParams:
     """cube3d/nn.hpp:119-124."""

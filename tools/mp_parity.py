@@ -173,6 +173,35 @@ def layer_check(cube, dims, name, dtype, mode):
     report(f"layer-{name}-traffic-balanced", sent == recv, f"sent={sent} recv={recv}")
 
 
+def loss_check(cube, dims):
+    """3-D cross-entropy on the grid vs the (finite-difference-checked) oracle."""
+    q = dims[0] * dims[1] * dims[2]
+    batch, seq, h, v = 4, 64, 64, 256
+    r = np.random.default_rng(21)
+    x = r.uniform(-1, 1, (batch * seq, h))
+    w = r.uniform(-0.5, 0.5, (h, v))
+    b = r.uniform(-0.1, 0.1, v)
+    t = r.integers(0, v, batch * seq)
+    X = c3.activation_to_device(cube, x, batch, seq, 0, c3.F32)
+    d0 = c3.triple_for_group(0)
+    W = c3.shard_to_device(cube, w, c3.WEIGHT, c3.F32, d0)
+    B = c3.vector_to_device(cube, b, c3.F32)
+    head = c3.LinearParams(W, B, 0)
+    loss, sv = c3.cross_entropy_fwd(cube, X, head, torch.tensor(t, dtype=torch.int32),
+                                    c3.GroupState(0), c3.MODE_F32)
+    dx, dw, db = c3.cross_entropy_bwd(cube, sv, head, c3.MODE_F32)
+    torch.cuda.synchronize()
+    lo, cache = O.cross_entropy_fwd(x, w, b, t)
+    dxo, dwo, dbo = O.cross_entropy_bwd(cache)
+    losses = gather_all(float(loss.item()))
+    gdx = c3.activation_to_global(gather_all(to_np(dx.local)), batch, seq, h, 0, dims)
+    gdw = c3.collect(gather_all(to_np(dw.shard)), c3.WEIGHT, dims, h, v, d0)
+    gdb = c3.collect_diagonal(gather_all(to_np(db.shard)), dims, v)
+    ok = (all(abs(l - lo) / abs(lo) < 1e-5 for l in losses) and O.normwise_err(gdx, dxo) < 1e-5
+          and O.normwise_err(gdw, dwo) < 1e-5 and O.normwise_err(gdb, dbo) < 1e-5)
+    report(f"cross-entropy-f32-{q}ranks", ok, f"loss={losses[0]:.6f} oracle={lo:.6f}")
+
+
 def main():
     rank, world, local = cdist.init_process_group("nccl")
     torch.cuda.set_device(local)
@@ -182,6 +211,7 @@ def main():
     if os.environ.get("MP_SKIP_MATMUL") is None:
         matmul_checks(cube, dims)
     if dims[1] == dims[2]:
+        loss_check(cube, dims)
         for name in ("layer_toy", "layer_small"):
             layer_check(cube, dims, name, c3.F32, c3.MODE_F32)
             layer_check(cube, dims, name, c3.BF16, c3.MODE_AUTO)
