@@ -339,6 +339,16 @@ int c3d_layer_bwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_act
                   const c3d_saved* saved, const c3d_layer_params* p, c3d_activation* dx,
                   c3d_layer_params* grads, void* stream);
 
+/* transformer_stack_fwd/bwd (cube3d/transformer.hpp:150-176): `n_layers` layers
+ * applied in order (backward in reverse); `layers` / `grads` are arrays of n_layers. */
+int c3d_stack_fwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_activation* x,
+                  const c3d_layer_params* layers, int n_layers, int* group, c3d_activation* y,
+                  c3d_saved** saved, void* stream);
+int c3d_stack_bwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_activation* dy,
+                  const c3d_saved* saved, const c3d_layer_params* layers, int n_layers,
+                  c3d_activation* dx, c3d_layer_params* grads, void* stream);
+
+
 #ifdef __cplusplus
 }
 #endif

@@ -130,6 +130,10 @@ SIGNATURES = {
                        P(c3d_activation), P(VP), VP],
     "c3d_linear_bwd": [VP, C.c_int, P(c3d_activation), VP, P(c3d_linear_params),
                        P(c3d_activation), P(c3d_matrix), P(c3d_vector), VP],
+    "c3d_stack_fwd": [VP, C.c_int, P(c3d_config), P(c3d_activation), P(c3d_layer_params),
+                      C.c_int, P(C.c_int), P(c3d_activation), P(VP), VP],
+    "c3d_stack_bwd": [VP, C.c_int, P(c3d_config), P(c3d_activation), VP, P(c3d_layer_params),
+                      C.c_int, P(c3d_activation), P(c3d_layer_params), VP],
     "c3d_loss_fwd": [VP, C.c_int, P(c3d_activation), P(c3d_linear_params), VP, P(C.c_int), VP,
                      P(VP), VP],
     "c3d_loss_bwd": [VP, C.c_int, VP, P(c3d_linear_params), P(c3d_activation), P(c3d_matrix),

@@ -28,7 +28,7 @@ struct c3d_rng {
 
 struct c3d_saved {
   std::unique_ptr<c3d::Saved> impl;
-  int kind = 0;  // 1 linear, 2 layernorm, 3 attention, 4 mlp, 5 layer, 6 loss
+  int kind = 0;  // 1 linear, 2 layernorm, 3 attention, 4 mlp, 5 layer, 6 loss, 7 stack
   int mode = 0;
 };
 
@@ -781,6 +781,52 @@ int c3d_layer_bwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_act
     c3d::layer_bwd(cb, mode, cfg_of(cfg), dya, sv, lp, dxa, g, as_stream(stream));
     act_out(dxa, dx);
     grads_out(g, grads);
+  });
+}
+
+int c3d_stack_fwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_activation* x,
+                  const c3d_layer_params* layers, int n_layers, int* group, c3d_activation* y,
+                  c3d_saved** saved, void* stream) {
+  return guard([&] {
+    need(x, "x");
+    need(layers, "layers");
+    need(group, "group");
+    need(y, "y");
+    need(saved, "saved");
+    if (n_layers < 1) c3d::fail(C3D_ERR_CONFIG_INVALID, "n_layers must be >= 1");
+    auto& cb = get(cube);
+    c3d::Act xa = act_of(cb, *x), ya = act_dest(y);
+    std::vector<c3d::LayerP> ps;
+    for (int i = 0; i < n_layers; ++i) ps.push_back(layer_of(cb, layers[i]));
+    auto sv = std::make_unique<c3d::StackSaved>();
+    c3d::stack_fwd(cb, mode, cfg_of(cfg), xa, ps, *group, ya, sv.get(), as_stream(stream));
+    act_out(ya, y);
+    auto h = std::make_unique<c3d_saved>();
+    h->kind = 7;
+    h->impl = std::move(sv);
+    *saved = h.release();
+  });
+}
+int c3d_stack_bwd(c3d_cube* cube, int mode, const c3d_config* cfg, const c3d_activation* dy,
+                  const c3d_saved* saved, const c3d_layer_params* layers, int n_layers,
+                  c3d_activation* dx, c3d_layer_params* grads, void* stream) {
+  return guard([&] {
+    need(dy, "dy");
+    need(layers, "layers");
+    need(dx, "dx");
+    need(grads, "grads");
+    auto& cb = get(cube);
+    auto& sv = saved_as<c3d::StackSaved>(saved, 7);
+    c3d::Act dya = act_of(cb, *dy), dxa = act_dest(dx);
+    std::vector<c3d::LayerP> ps;
+    std::vector<c3d::LayerG> gs;
+    for (int i = 0; i < n_layers; ++i) {
+      ps.push_back(layer_of(cb, layers[i]));
+      gs.push_back(grads_of(grads[i]));
+    }
+    c3d::stack_bwd(cb, mode, cfg_of(cfg), dya, sv, ps, dxa, gs, as_stream(stream));
+    act_out(dxa, dx);
+    for (int i = 0; i < n_layers; ++i) grads_out(gs[i], &grads[i]);
   });
 }
 

@@ -781,3 +781,54 @@ void loss_bwd(Cube& cube, int mode, const LossSaved& sv, const LinearP& head, Ac
 }
 
 }  // namespace c3d
+
+namespace c3d {
+
+// ------------------------------------------------------------------ stack
+
+void stack_fwd(Cube& cube, int mode, const Config& cfg, const Act& x,
+               const std::vector<LayerP>& ps, int& group, Act& y, StackSaved* sv,
+               cudaStream_t s) {
+  if (ps.empty()) fail(C3D_ERR_CONFIG_INVALID, "a stack needs at least one layer");
+  if (!sv) fail(C3D_ERR_CONFIG_INVALID, "stack forward needs saved state");
+  const size_t bytes = x.elems() * dtype_size(x.dtype);
+  Act cur = x;
+  for (size_t i = 0; i < ps.size(); ++i) {
+    Act out;
+    if (i + 1 == ps.size()) {
+      out = y;
+    } else {
+      out.data = sv->keep(DevBuf(bytes, s)).get();
+      out.dtype = x.dtype;
+    }
+    sv->layers.push_back(std::make_unique<LayerSaved>());
+    layer_fwd(cube, mode, cfg, cur, ps[i], group, out, sv->layers.back().get(), s);
+    cur = out;
+  }
+  y = cur;
+}
+
+void stack_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const StackSaved& sv,
+               const std::vector<LayerP>& ps, Act& dx, std::vector<LayerG>& gs, cudaStream_t s) {
+  if (ps.size() != sv.layers.size() || gs.size() != ps.size())
+    fail(C3D_ERR_CONFIG_INVALID, "stack backward: layer count differs from the forward");
+  const size_t bytes = dy.elems() * dtype_size(dy.dtype);
+  DevBuf tmp[2];
+  Act cur = dy;
+  for (size_t k = ps.size(); k-- > 0;) {
+    Act out;
+    if (k == 0) {
+      out = dx;
+    } else {
+      DevBuf& b = tmp[k % 2];
+      b = DevBuf(bytes, s);
+      out.data = b.get();
+      out.dtype = dy.dtype;
+    }
+    layer_bwd(cube, mode, cfg, cur, *sv.layers[k], ps[k], out, gs[k], s);
+    cur = out;
+  }
+  dx = cur;
+}
+
+}  // namespace c3d

@@ -157,6 +157,17 @@ void mlp_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const MlpSa
              const Operand* fc1_wg = nullptr, const Operand* fc2_wg = nullptr,
              const LinearSinks* fc1_sinks = nullptr, const LinearSinks* fc2_sinks = nullptr);
 
+// transformer_stack_fwd/bwd (cube3d/transformer.hpp:150-176): the layer loop, the
+// backward in reverse. Intermediate activations are owned by the saved state.
+struct StackSaved : Saved {
+  std::vector<std::unique_ptr<LayerSaved>> layers;
+};
+void stack_fwd(Cube& cube, int mode, const Config& cfg, const Act& x,
+               const std::vector<LayerP>& ps, int& group, Act& y, StackSaved* saved,
+               cudaStream_t s);
+void stack_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const StackSaved& sv,
+               const std::vector<LayerP>& ps, Act& dx, std::vector<LayerG>& gs, cudaStream_t s);
+
 // Mean cross-entropy of softmax(x W + b) against global token targets (int32 [batch *
 // seq], device); `loss` is one device float (identical on every rank). `targets` must
 // stay valid until loss_bwd.

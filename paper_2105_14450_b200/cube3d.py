@@ -750,6 +750,34 @@ def transformer_layer_bwd(cube: Cube, dy: Activation3D, saved: Saved, params: La
     return dx, grads
 
 
+def transformer_stack_fwd(cube: Cube, x: Activation3D, layers: Sequence["LayerParams"],
+                          cfg: TransformerConfig, gs: GroupState, mode=MODE_AUTO, stream=None):
+    """cube3d/transformer.hpp:150-163 -> (y, saved)."""
+    y = _act_out(cube, x.batch, x.seq, x.hidden, x.group, c3d_dtype(x.local))
+    arr = (L.c3d_layer_params * len(layers))(*[p.c() for p in layers])
+    cx, cy, cc = x.c(), y.c(), cfg.c()
+    g = C.c_int(gs.input_group)
+    h = C.c_void_p()
+    call("c3d_stack_fwd", cube.handle, mode, C.byref(cc), C.byref(cx), arr, len(layers),
+         C.byref(g), C.byref(cy), C.byref(h), _stream(stream))
+    gs.input_group = g.value
+    return y, Saved(h)
+
+
+def transformer_stack_bwd(cube: Cube, dy: Activation3D, saved: Saved, layers: Sequence["LayerParams"],
+                          cfg: TransformerConfig, mode=MODE_AUTO, grad_dtype: Optional[int] = None,
+                          stream=None):
+    """cube3d/transformer.hpp:165-176 (reverse order) -> (dx, [grads per layer])."""
+    dx = _act_out(cube, dy.batch, dy.seq, dy.hidden, dy.group, c3d_dtype(dy.local))
+    grads = [empty_like_params(cube, p, grad_dtype) for p in layers]
+    arr = (L.c3d_layer_params * len(layers))(*[p.c() for p in layers])
+    garr = (L.c3d_layer_params * len(layers))(*[g.c() for g in grads])
+    cdy, cdx, cc = dy.c(), dx.c(), cfg.c()
+    call("c3d_stack_bwd", cube.handle, mode, C.byref(cc), C.byref(cdy), saved._h, arr, len(layers),
+         C.byref(cdx), garr, _stream(stream))
+    return dx, grads
+
+
 def _block_fwd(name, cube, x, params, cfg, gs, mode, stream):
     y = _act_out(cube, x.batch, x.seq, x.hidden, x.group, c3d_dtype(x.local))
     cx, cy, cp, cc = x.c(), y.c(), params.c(), cfg.c()

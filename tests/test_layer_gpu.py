@@ -147,3 +147,40 @@ def test_layer_config_errors(cube):
         c3.transformer_layer_fwd(cube, X, params, c3.TransformerConfig(2, 8, 2, 16),
                                  c3.GroupState(1))
     assert e.value.name == "GroupMismatch"
+
+
+@pytest.mark.parametrize("dtype,mode", [("f32", "f32"), ("bf16", "auto")])
+def test_transformer_stack_two_layers(cube, dtype, mode):
+    """transformer_stack_fwd/bwd (cube3d/transformer.hpp:150-176): two layers against the
+    oracle's layer composition (the reference's 2-layer stack KAT,
+    tests/test_nn_layers.cpp:497-528, checks the same composition against serial)."""
+    import torch
+    b, s, n, h = 2, 128, 4, 256
+    dt = c3.F32 if dtype == "f32" else c3.BF16
+    md = c3.MODE_F32 if mode == "f32" else c3.MODE_AUTO
+    rnd = (lambda a: a) if dtype == "f32" else bf16_round
+    P = [O.init_layer_params(h, 31), O.init_layer_params(h, 32)]
+    gps = [c3.GlobalLayerParams(**{f: rnd(getattr(p, f)) for f in O.FIELDS}) for p in P]
+    r = O.Rng(5)
+    x = rnd(O.random_matrix(b * s, h, r))
+    dy = rnd(O.random_matrix(b * s, h, r))
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params = [c3.partition_layer_params(cube, gp, 0, dt) for gp in gps]
+    X = c3.activation_to_device(cube, x, b, s, 0, dt)
+    DY = c3.activation_to_device(cube, dy, b, s, 0, dt)
+    gs = c3.GroupState(0)
+    y, sv = c3.transformer_stack_fwd(cube, X, params, cfg, gs, md)
+    dx, grads = c3.transformer_stack_bwd(cube, DY, sv, params, cfg, md, grad_dtype=c3.F32)
+    torch.cuda.synchronize()
+    PO = [oracle_params(gp) for gp in gps]
+    y1, c1 = O.layer_fwd(x, PO[0], b, s, n)
+    y2, c2 = O.layer_fwd(y1, PO[1], b, s, n)
+    d1, G2 = O.layer_bwd(dy, c2, PO[1], b, s, n)
+    d0, G1 = O.layer_bwd(d1, c1, PO[0], b, s, n)
+    tol = TOL_F32_NORM if dtype == "f32" else 2e-2
+    assert O.normwise_err(to_np(y.local), y2) < tol
+    assert O.normwise_err(to_np(dx.local), d0) < tol
+    for k, G in ((0, G1), (1, G2)):
+        for f in O.FIELDS:
+            got = to_np(getattr(grads[k], f).shard)
+            assert O.normwise_err(got, getattr(G, f).reshape(got.shape)) < tol, (k, f)
