@@ -162,6 +162,46 @@ def reference_arm(args, wl):
     return 0
 
 
+# ------------------------------------------------------------ 3-D matmul line
+def matmul_tflops(cube, n=8192, iters=20):
+    """BASELINE.json's other headline: 3-D matmul C = A B (matmul_ab_fwd,
+    cube3d/ops3d.hpp:114-132) at M=N=K=n in bf16 tensor-core mode on the same grid,
+    device-resident, captured as a graph; whole-job TFLOP/s (2 n^3 / time, max over
+    ranks)."""
+    import torch
+    from paper_2105_14450_b200 import cube3d as c3
+    from paper_2105_14450_b200 import dist
+    dev = cube.device_str()
+    g = torch.Generator(device=dev).manual_seed(99 + cube.rank)
+    d = c3.canonical_directions()
+
+    def mat(layout):
+        shp = cube.local_shape(layout, n, n, d)
+        t = (torch.rand(shp, device=dev, generator=g) - 0.5).to(torch.bfloat16)
+        return c3.ShardedMatrix(t, n, n, layout, d)
+
+    a, b = mat(c3.INPUT), mat(c3.WEIGHT)
+    for _ in range(3):
+        c3.matmul_ab_fwd(cube, a, b)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        for _ in range(iters):
+            c3.matmul_ab_fwd(cube, a, b)
+    gr.replay()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = dist.max_over_ranks(e0.elapsed_time(e1) / iters)
+    return {"m_n_k": n, "tflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e12, "ms": ms,
+            "grid": "x".join(map(str, cube.dims)), "dtype": "bf16 (fp32 accumulate)",
+            "path": "c3d_matmul_ab_fwd: all-gathers + tcgen05 GEMM + fused reduce-scatter"}
+
+
 # ------------------------------------------------------------ end-to-end arm
 def e2e_pipelined(args, b, x, dy, step, stream, world):
     """End to end through the public API with host buffers: every step copies its x and
@@ -292,7 +332,7 @@ def our_arm(args, wl):
     torch.cuda.set_device(local)
     if world != args.gpus:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}")
-    cube = dist.make_cube()
+    cube = dist.make_cube(tuple(int(v) for v in args.grid.split("x")) if args.grid else None)
     b, s, n, h = wl["b"], wl["s"], wl["n"], wl["h"]
     cfg = c3.TransformerConfig(b, s, n, h)
     params, x, dy = make_layer_inputs(cube, wl, c3.BF16)
@@ -409,6 +449,13 @@ def our_arm(args, wl):
     if not args.no_e2e:
         e2e = e2e_pipelined(args, b, x, dy, step, stream, world)
 
+    mm = None
+    if not args.no_matmul:
+        try:
+            mm = matmul_tflops(cube)
+        except Exception as ex:  # report, never fake
+            mm = {"error": str(ex)}
+
     # ---- roofline of the dominant kernel (tcgen05 GEMM), live per-launch timing
     peak_tc, peak_hbm, peak_src = measured_peaks()
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
@@ -458,6 +505,7 @@ def our_arm(args, wl):
                                     "(last of K replays)" if prof_src == "graph" else
                                     f"per-launch CUDA events over {args.steps} eager steps")},
             "layer_tflops": layer_tflops,
+            "matmul": mm,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
             "collectives": {"calls_per_step": comm_n / prof_steps,
                             "ms_per_step": comm_ms / prof_steps,
@@ -488,6 +536,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-matmul", action="store_true", help="skip the 3-D matmul TFLOP/s line")
+    ap.add_argument("--grid", default=None,
+                    help="px x py x pz (e.g. 4x1x1); default: 1x1x1, 2x1x1, 1x2x2, 2x2x2")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
