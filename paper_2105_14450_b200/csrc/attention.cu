@@ -244,6 +244,190 @@ void launch_attn(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& 
   kern<<<dim3(a.S / kQ, nslices), kThreadsAttn, smem, s>>>(q, k, v, p, a);
 }
 
+
+// ---------------------------------------------------------------- backward (dS, dQ)
+// Per (slice, 128-query tile): dP = dO V^T in TMEM (keys fp32 columns); the saved P
+// tile arrives by TMA into shared memory (UMMA K-major layout); 16 warps form
+// dS = P * (dP - D) * scale in place (D = sum_j P dP = rowsum(dO * O), precomputed),
+// dS goes to HBM (TMA store, for dK = dS^T Q) and stays in shared memory as the A
+// operand of dQ = dS K (K staged MN-major into the buffer V used). Replaces the dS
+// GEMM (with its fused softmax-backward epilogue) and the dQ GEMM of attention_bwd.
+struct AttnBwdArgs {
+  int S, keys, H;
+  float scale;
+  const float* rowdot;  // D per (slice, query)
+  __nv_bfloat16* dq;
+  long long dq_sr, dq_sb_lo, dq_sb_hi;
+};
+
+template <int KEYS>
+__global__ void __launch_bounds__(kThreadsAttn, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tmDO, const __grid_constant__ CUtensorMap tmV,
+                    const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmP,
+                    const __grid_constant__ CUtensorMap tmDS, const AttnBwdArgs args) {
+  constexpr int kOBytes = kQ * kDh * 2;          // dO tile, 16 KB
+  constexpr int kVBytes = KEYS * kDh * 2;        // V (then K), keys x 128 B
+  constexpr int kPBytes = KEYS / 64 * kQ * 128;  // P / dS chunks
+  constexpr uint32_t kIdescP = ptx::idesc_bf16_f32(kQ, 256, false, false);
+  constexpr uint32_t kIdescQ = ptx::idesc_bf16_f32(kQ, kDh, false, true);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sO = smem;
+  uint8_t* sV = smem + kOBytes;  // V, then K (MN-major)
+  uint8_t* sP = smem + kOBytes + kVBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint64_t* bar_a = bars;      // dO + V
+  uint64_t* bar_p = bars + 1;  // P
+  uint64_t* bar_s = bars + 2;  // dP in TMEM
+  uint64_t* bar_k = bars + 3;  // K
+  uint64_t* bar_ds = bars + 4; // dS in shared memory
+  uint64_t* bar_o = bars + 5;  // dQ in TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int q0 = blockIdx.x * kQ;
+  const int b = blockIdx.y;
+  const int c3 = b % args.H, c4 = b / args.H;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 6; ++i) ptx::mbar_init(bars + i, i == 4 ? 32 * kSoftWarps : 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::mbar_arrive_expect_tx(bar_a, kOBytes + kVBytes);
+      ptx::tma_load_5d(sO, &tmDO, bar_a, 0, q0, 0, c3, c4);
+#pragma unroll
+      for (int h = 0; h < KEYS / 256; ++h)
+        ptx::tma_load_5d(sV + h * 256 * 128, &tmV, bar_a, 0, h * 256, 0, c3, c4);
+      ptx::mbar_arrive_expect_tx(bar_p, kPBytes);
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+        ptx::tma_load_5d(sP + kb * 16384, &tmP, bar_p, kb * 64, q0, 0, c3, c4);
+      // K replaces V once the dP product has consumed it
+      ptx::mbar_wait(bar_s, 0);
+      ptx::mbar_arrive_expect_tx(bar_k, kVBytes);
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+        ptx::tma_load_5d(sV + kb * 8192, &tmK, bar_k, 0, kb * 64, 0, c3, c4);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      ptx::mbar_wait(bar_a, 0);
+      ptx::tc_fence_after();
+      const uint32_t oa = ptx::smem_u32(sO), va = ptx::smem_u32(sV);
+#pragma unroll
+      for (int h = 0; h < KEYS / 256; ++h)
+#pragma unroll
+        for (int k = 0; k < kDh / 16; ++k)
+          ptx::umma_bf16(tmem + h * 256, ptx::smem_desc_sw128(oa + 32 * k, 16, 1024),
+                         ptx::smem_desc_sw128(va + h * 256 * 128 + 32 * k, 16, 1024), kIdescP,
+                         k > 0 ? 1u : 0u);
+      ptx::umma_commit(bar_s);
+      ptx::mbar_wait(bar_ds, 0);
+      ptx::mbar_wait(bar_k, 0);
+      ptx::tc_fence_after();
+      const uint32_t pa = ptx::smem_u32(sP), ka = ptx::smem_u32(sV);
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          ptx::umma_bf16(tmem, ptx::smem_desc_sw128(pa + kb * 16384 + 32 * k, 16, 1024),
+                         ptx::smem_desc_sw128(ka + kb * 8192 + 2048 * k, 8192, 1024), kIdescQ,
+                         (kb > 0 || k > 0) ? 1u : 0u);
+      ptx::umma_commit(bar_o);
+    }
+  } else {
+    constexpr int kGroupCols = KEYS / 4;
+    const int quarter = warp & 3;
+    const int group = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const int c0 = group * kGroupCols;
+    const float sd = args.scale * __ldg(args.rowdot + static_cast<long long>(b) * args.S + q0 + row);
+    ptx::mbar_wait(bar_p, 0);
+    ptx::mbar_wait(bar_s, 0);
+    ptx::tc_fence_after();
+#pragma unroll 1
+    for (int c = c0; c < c0 + kGroupCols; c += 32) {
+      float v[32];
+      ptx::tmem_ld32(trow + c, v);
+      uint8_t* chunk_row = sP + (c >> 6) * 16384 + row * 128;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int chunk = ((c >> 5) & 1) * 4 + j;
+        uint4* ptr = reinterpret_cast<uint4*>(chunk_row + ((chunk ^ (row & 7)) << 4));
+        uint4 pk = *ptr;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 pp = __bfloat1622float2(h[i]);
+          h[i] = __floats2bfloat162_rn(pp.x * fmaf(v[8 * j + 2 * i], args.scale, -sd),
+                                       pp.y * fmaf(v[8 * j + 2 * i + 1], args.scale, -sd));
+        }
+        *ptr = pk;
+      }
+    }
+    // dS visible to the tensor core; dP columns free for dQ
+    ptx::fence_async_smem();
+    ptx::tc_fence_before();
+    ptx::mbar_arrive(bar_ds);
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
+    if (warp == 2 && lane == 0) {
+#pragma unroll
+      for (int kb = 0; kb < KEYS / 64; ++kb)
+        ptx::tma_store_5d(&tmDS, sP + kb * 16384, kb * 64, q0, 0, c3, c4);
+      ptx::bulk_commit();
+    }
+    if (group < 2) {
+      ptx::mbar_wait(bar_o, 0);
+      ptx::tc_fence_after();
+      float o[32];
+      ptx::tmem_ld32(trow + group * 32, o);
+      __nv_bfloat16* dst = args.dq + c3 * args.dq_sb_lo + c4 * args.dq_sb_hi +
+                           static_cast<long long>(q0 + row) * args.dq_sr + group * 32;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 pk;
+        pk.x = pack_bf16(o[8 * j + 0], o[8 * j + 1]);
+        pk.y = pack_bf16(o[8 * j + 2], o[8 * j + 3]);
+        pk.z = pack_bf16(o[8 * j + 4], o[8 * j + 5]);
+        pk.w = pack_bf16(o[8 * j + 6], o[8 * j + 7]);
+        reinterpret_cast<uint4*>(dst)[j] = pk;
+      }
+    }
+    if (warp == 2 && lane == 0) ptx::bulk_wait_all();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int KEYS>
+void launch_attn_bwd(const CUtensorMap& o, const CUtensorMap& v, const CUtensorMap& k,
+                     const CUtensorMap& p, const CUtensorMap& ds, const AttnBwdArgs& a, int nslices,
+                     cudaStream_t s) {
+  constexpr int smem = 1024 + kQ * kDh * 2 + KEYS * kDh * 2 + KEYS / 64 * kQ * 128 + 64;
+  auto kern = attn_bwd_kernel<KEYS>;
+  static bool attr = false;
+  if (!attr) {
+    C3D_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  kern<<<dim3(a.S / kQ, nslices), kThreadsAttn, smem, s>>>(o, v, k, p, ds, a);
+}
+
 }  // namespace
 
 bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
@@ -280,6 +464,46 @@ bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& pro
   if (keys == 512) launch_attn<512>(mq, mk, mv, mp, a, nslices, s);
   else launch_attn<256>(mq, mk, mv, mp, a, nslices, s);
   check_launch("attn_fwd_fused");
+  return true;
+}
+
+}  // namespace c3d
+
+namespace c3d {
+
+bool attn_bwd_fused(const View& d_o, const View& v, const View& k_mn, const View& probs,
+                    const View& ds, const View& dq, const float* rowdot, int64_t S, int64_t keys,
+                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s) {
+  if (std::getenv("C3D_NO_FUSED_ATTN") || std::getenv("C3D_NO_FUSED_ATTN_BWD")) return false;
+  if (dh != kDh || S % kQ || (keys != 256 && keys != 512) || H <= 0 || !rowdot) return false;
+  for (const View* w : {&d_o, &v, &k_mn, &probs, &ds, &dq}) {
+    if (w->dtype != kBF16 || reinterpret_cast<uintptr_t>(w->base) % 16) return false;
+    if (w->rsplit || w->csplit || w->b_lo_n != H) return false;
+  }
+  if (dq.sc != 1 || (dq.sr * 2) % 16 || (dq.sb_lo * 2) % 16 || (dq.sb_hi * 2) % 16) return false;
+  int mn = 0;
+  const CUtensorMap mo = tc_operand_map(d_o, S, dh, nslices, kQ, &mn);
+  if (mn) return false;
+  const CUtensorMap mv = tc_operand_map(v, keys, dh, nslices, 256, &mn);
+  if (mn) return false;
+  const CUtensorMap mk = tc_operand_map(k_mn, dh, keys, nslices, 64, &mn);
+  if (!mn) return false;
+  CUtensorMap mp, mds;
+  if (!tc_store_map(probs, S, keys, nslices, 64, kQ, &mp)) return false;
+  if (!tc_store_map(ds, S, keys, nslices, 64, kQ, &mds)) return false;
+  AttnBwdArgs a{};
+  a.S = static_cast<int>(S);
+  a.keys = static_cast<int>(keys);
+  a.H = static_cast<int>(H);
+  a.scale = scale;
+  a.rowdot = rowdot;
+  a.dq = static_cast<__nv_bfloat16*>(dq.base);
+  a.dq_sr = dq.sr;
+  a.dq_sb_lo = dq.sb_lo;
+  a.dq_sb_hi = dq.sb_hi;
+  if (keys == 512) launch_attn_bwd<512>(mo, mv, mk, mp, mds, a, nslices, s);
+  else launch_attn_bwd<256>(mo, mv, mk, mp, mds, a, nslices, s);
+  check_launch("attn_bwd_fused");
   return true;
 }
 

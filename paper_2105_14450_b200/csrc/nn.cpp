@@ -426,7 +426,19 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
   const bool fused_ds = a.Ps == 1 && mode != C3D_MODE_F32 && dt == kBF16 &&
                         !std::getenv("C3D_NO_FUSED_ATTN");
   DevBuf dpf;
+  bool fused_dq = false;  // dS and dQ from the fused attention-backward kernel
   if (fused_ds) {
+    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
+    k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
+                  rd.as<float>(), s);
+    fused_dq = attn_bwd_fused(packed_view(dcf.ptr, dt, a, false), qkv_view(qkv, dt, a, 2, false),
+                              qkv_view(qkv, dt, a, 1, true), scores_view(S.probs, dt, a, false),
+                              scores_view(dp.get(), dt, a, false),
+                              qkv_view(dqkv_buf.get(), dt, a, 0, false), rd.as<float>(), a.S, a.sl,
+                              a.dh, a.H, nslices, a.scale, s);
+    if (fused_dq) cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+  }
+  if (fused_ds && !fused_dq) {
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
     k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
                   rd.as<float>(), s);
@@ -440,7 +452,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
     e.rv_div = a.sl;
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
                qkv_view(qkv, dt, a, 2, false), e, s);
-  } else {
+  } else if (!fused_ds) {
     // dP = dctx_full V^T (fp32)
     dpf = DevBuf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
@@ -467,7 +479,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                      dp.get(), dt, s);
   }
   // dQ = dS K (reduce-scattered), dK = dS^T Q_full
-  {
+  if (!fused_dq) {
     Epilogue e;
     DevBuf partial;
     if (a.Ps == 1) {

@@ -184,3 +184,21 @@ def test_transformer_stack_two_layers(cube, dtype, mode):
         for f in O.FIELDS:
             got = to_np(getattr(grads[k], f).shard)
             assert O.normwise_err(got, getattr(G, f).reshape(got.shape)) < tol, (k, f)
+
+
+def test_fused_attention_backward_matches_gemm_path(cube, monkeypatch):
+    """The fused attention-backward kernel (dP in TMEM, dS in place, dQ = dS K) against the
+    GEMM path with the softmax backward in the dP epilogue, same inputs."""
+    b, s, n, h = 2, 512, 8, 512
+    r = O.Rng(23)
+    P = O.init_layer_params(h, 23)
+    gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
+    x = bf16_round(O.random_matrix(b * s, h, r))
+    dy = bf16_round(O.random_matrix(b * s, h, r))
+    fused = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    monkeypatch.setenv("C3D_NO_FUSED_ATTN_BWD", "1")
+    plain = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    assert np.array_equal(fused[0], plain[0])
+    assert O.normwise_err(fused[1], plain[1]) < 5e-3
+    for f in O.FIELDS:
+        assert O.normwise_err(fused[2][f], plain[2][f]) < 5e-3, f
