@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "common.hpp"
 #include "gemm.hpp"
@@ -34,11 +35,19 @@ constexpr int kDh = 64;   // head dim (one 128-B K block)
 constexpr int kSoftWarps = 16;     // 4 TMEM lane quarters x 4 column groups
 constexpr int kThreadsAttn = 64 + 32 * kSoftWarps;  // warp 0 TMA, warp 1 MMA, softmax warps
 
+// Modes: 0 whole softmax on this rank; with the key range split along the seq axis
+// (distributed softmax, cube3d/attention.hpp:106-126): 1 local row max of S -> stat_max,
+// 2 sum exp(scale (S - M)) with the all-reduced max M -> stat_sum, 3 P = exp(.) / L
+// with both all-reduced, stored, and the partial context P V.
 struct AttnArgs {
   int S, keys, H;
   float scale_log2;  // scale * log2(e)
+  int q_split;       // rows per gathered query block (0: not split)
   __nv_bfloat16* ctx;
   long long ctx_sr, ctx_sb_lo, ctx_sb_hi;  // element strides of the context view
+  long long ctx_split, ctx_s_hi;           // split rows of the (partial) context view
+  float* stat_max;   // [slice][S]
+  float* stat_sum;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -46,7 +55,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int KEYS>
+template <int KEYS, int MODE>
 __global__ void __launch_bounds__(kThreadsAttn, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmP,
@@ -97,14 +106,18 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(bar_qk, kQBytes + kKBytes);
-      ptx::tma_load_5d(sQ, &tmQ, bar_qk, 0, q0, 0, c3, c4);
+      const int qr = args.q_split ? q0 % args.q_split : q0;
+      const int qh = args.q_split ? q0 / args.q_split : 0;
+      ptx::tma_load_5d(sQ, &tmQ, bar_qk, 0, qr, qh, c3, c4);
 #pragma unroll
       for (int h = 0; h < KEYS / 256; ++h)
         ptx::tma_load_5d(sK + h * 256 * 128, &tmK, bar_qk, 0, h * 256, 0, c3, c4);
-      ptx::mbar_arrive_expect_tx(bar_v, kVBytes);
+      if (MODE == 0 || MODE == 3) {
+        ptx::mbar_arrive_expect_tx(bar_v, kVBytes);
 #pragma unroll
-      for (int kb = 0; kb < KEYS / 64; ++kb)
-        ptx::tma_load_5d(sV + kb * 8192, &tmV, bar_v, 0, kb * 64, 0, c3, c4);
+        for (int kb = 0; kb < KEYS / 64; ++kb)
+          ptx::tma_load_5d(sV + kb * 8192, &tmV, bar_v, 0, kb * 64, 0, c3, c4);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -119,6 +132,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
                          ptx::smem_desc_sw128(ka + h * 256 * 128 + 32 * k, 16, 1024), kIdescS,
                          k > 0 ? 1u : 0u);
       ptx::umma_commit(bar_s);
+      if (MODE == 0 || MODE == 3) {  // modes 1, 2: statistics only, no O
       // O = P V once the softmax warps have written P and released the S columns
       ptx::mbar_wait(bar_p, 0);
       ptx::mbar_wait(bar_v, 0);
@@ -132,6 +146,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
                          ptx::smem_desc_sw128(va + kb * 8192 + 2048 * k, 8192, 1024), kIdescO,
                          (kb > 0 || k > 0) ? 1u : 0u);
       ptx::umma_commit(bar_o);
+      }
     }
   } else {
     // ---------------- softmax: warp w owns TMEM lanes 32*(w % 4) .. +32 and column group
@@ -144,29 +159,43 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
     const int c0 = group * kGroupCols;
     ptx::mbar_wait(bar_s, 0);
     ptx::tc_fence_after();
+    const long long srow = static_cast<long long>(b) * args.S + q0 + row;  // [slice][S]
     float m = -INFINITY;
+    if (MODE == 2 || MODE == 3) {
+      m = __ldg(args.stat_max + srow);  // all-reduced along the seq axis
+    } else {
 #pragma unroll 1
-    for (int c = c0; c < c0 + kGroupCols; c += 32) {
-      float v[32];
-      ptx::tmem_ld32(trow + c, v);
+      for (int c = c0; c < c0 + kGroupCols; c += 32) {
+        float v[32];
+        ptx::tmem_ld32(trow + c, v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) m = fmaxf(m, v[j]);
+        for (int j = 0; j < 32; ++j) m = fmaxf(m, v[j]);
+      }
+      red[group * kQ + row] = m;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
+      m = fmaxf(fmaxf(red[row], red[kQ + row]), fmaxf(red[2 * kQ + row], red[3 * kQ + row]));
+      if (MODE == 1) {
+        if (group == 0) args.stat_max[srow] = m;
+      }
     }
-    red[group * kQ + row] = m;
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
-    m = fmaxf(fmaxf(red[row], red[kQ + row]), fmaxf(red[2 * kQ + row], red[3 * kQ + row]));
     const float ms = m * args.scale_log2;
     float sum = 0.f;
+    if (MODE == 3) {
+      sum = __ldg(args.stat_sum + srow);
+    } else if (MODE != 1) {
 #pragma unroll 1
-    for (int c = c0; c < c0 + kGroupCols; c += 32) {
-      float v[32];
-      ptx::tmem_ld32(trow + c, v);
+      for (int c = c0; c < c0 + kGroupCols; c += 32) {
+        float v[32];
+        ptx::tmem_ld32(trow + c, v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(v[j], args.scale_log2, -ms));
+        for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(v[j], args.scale_log2, -ms));
+      }
+      red[4 * kQ + group * kQ + row] = sum;
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
+      sum = (red[4 * kQ + row] + red[5 * kQ + row]) + (red[6 * kQ + row] + red[7 * kQ + row]);
+      if (MODE == 2 && group == 0) args.stat_sum[srow] = sum;
     }
-    red[4 * kQ + group * kQ + row] = sum;
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
-    sum = (red[4 * kQ + row] + red[5 * kQ + row]) + (red[6 * kQ + row] + red[7 * kQ + row]);
+    if (MODE == 0 || MODE == 3) {
     const float inv = 1.f / sum;
 #pragma unroll 1
     for (int c = c0; c < c0 + kGroupCols; c += 32) {
@@ -206,8 +235,11 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
       ptx::tc_fence_after();
       float o[32];
       ptx::tmem_ld32(trow + group * 32, o);
-      __nv_bfloat16* dst = args.ctx + c3 * args.ctx_sb_lo + c4 * args.ctx_sb_hi +
-                           static_cast<long long>(q0 + row) * args.ctx_sr + group * 32;
+      const long long q = q0 + row;
+      const long long qoff = args.ctx_split ? (q % args.ctx_split) * args.ctx_sr +
+                                                  (q / args.ctx_split) * args.ctx_s_hi
+                                            : q * args.ctx_sr;
+      __nv_bfloat16* dst = args.ctx + c3 * args.ctx_sb_lo + c4 * args.ctx_sb_hi + qoff + group * 32;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 pk;
@@ -219,6 +251,7 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
       }
     }
     if (warp == 2 && lane == 0) ptx::bulk_wait_all();
+    }  // MODE 0 / 3
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -228,14 +261,14 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
   }
 }
 
-template <int KEYS>
+template <int KEYS, int MODE>
 void launch_attn(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& v,
                  const CUtensorMap& p, const AttnArgs& a, int nslices, cudaStream_t s) {
   constexpr int kQBytes = kQ * kDh * 2, kKBytes = KEYS * kDh * 2;
   constexpr int kPBytes = KEYS / 64 * kQ * 128;
   constexpr int kVOff = (kQBytes + kKBytes > kPBytes ? kQBytes + kKBytes : kPBytes);
   constexpr int smem = 1024 + kVOff + KEYS * kDh * 2 + 64 + 8 * kQ * 4;
-  auto kern = attn_fwd_kernel<KEYS>;
+  auto kern = attn_fwd_kernel<KEYS, MODE>;
   static bool attr = false;
   if (!attr) {
     C3D_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -432,15 +465,18 @@ void launch_attn_bwd(const CUtensorMap& o, const CUtensorMap& v, const CUtensorM
 
 bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
                     int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
-                    cudaStream_t s) {
+                    cudaStream_t s, int mode, float* stat_max, float* stat_sum) {
   if (std::getenv("C3D_NO_FUSED_ATTN")) return false;
   if (dh != kDh || S % kQ || (keys != 256 && keys != 512) || H <= 0) return false;
+  if (mode < 0 || mode > 3 || (mode > 0 && (!stat_max || !stat_sum))) return false;
   for (const View* w : {&q, &k, &v, &probs, &ctx})
     if (w->dtype != kBF16 || reinterpret_cast<uintptr_t>(w->base) % 16) return false;
-  if (q.rsplit || q.csplit || k.rsplit || k.csplit || v.rsplit || v.csplit || probs.rsplit ||
-      probs.csplit || ctx.rsplit || ctx.csplit)
+  if (q.csplit || (q.rsplit && q.rsplit % kQ) || k.rsplit || k.csplit || v.rsplit || v.csplit ||
+      probs.rsplit || probs.csplit || ctx.csplit || (ctx.rsplit && ctx.rsplit % kQ))
     return false;
-  if (ctx.sc != 1 || (ctx.sr * 2) % 16 || (ctx.sb_lo * 2) % 16 || (ctx.sb_hi * 2) % 16) return false;
+  if (ctx.sc != 1 || (ctx.sr * 2) % 16 || (ctx.sb_lo * 2) % 16 || (ctx.sb_hi * 2) % 16 ||
+      (ctx.s_hi * 2) % 16)
+    return false;
   if (ctx.b_lo_n != H || q.b_lo_n != H || k.b_lo_n != H || v.b_lo_n != H || probs.b_lo_n != H)
     return false;
   int mn = 0;
@@ -457,12 +493,26 @@ bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& pro
   a.keys = static_cast<int>(keys);
   a.H = static_cast<int>(H);
   a.scale_log2 = scale * 1.4426950408889634f;
+  a.q_split = static_cast<int>(q.rsplit);
   a.ctx = static_cast<__nv_bfloat16*>(ctx.base);
   a.ctx_sr = ctx.sr;
   a.ctx_sb_lo = ctx.sb_lo;
   a.ctx_sb_hi = ctx.sb_hi;
-  if (keys == 512) launch_attn<512>(mq, mk, mv, mp, a, nslices, s);
-  else launch_attn<256>(mq, mk, mv, mp, a, nslices, s);
+  a.ctx_split = ctx.rsplit;
+  a.ctx_s_hi = ctx.s_hi;
+  a.stat_max = stat_max;
+  a.stat_sum = stat_sum;
+  auto go = [&](auto kk) {
+    constexpr int K = decltype(kk)::value;
+    switch (mode) {
+      case 0: launch_attn<K, 0>(mq, mk, mv, mp, a, nslices, s); break;
+      case 1: launch_attn<K, 1>(mq, mk, mv, mp, a, nslices, s); break;
+      case 2: launch_attn<K, 2>(mq, mk, mv, mp, a, nslices, s); break;
+      default: launch_attn<K, 3>(mq, mk, mv, mp, a, nslices, s); break;
+    }
+  };
+  if (keys == 512) go(std::integral_constant<int, 512>{});
+  else go(std::integral_constant<int, 256>{});
   check_launch("attn_fwd_fused");
   return true;
 }

@@ -360,7 +360,30 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
                                     packed_out(ctx.data, dt, a, false), a.S, a.sl, a.dh, a.H,
                                     nslices, a.scale, s);
   if (fused) cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
-  if (!fused) {
+  // key range split along the seq axis: the distributed softmax of the reference
+  // (row max -> all-reduce(max) -> exp-sum -> all-reduce(sum) -> normalise) with the
+  // scores recomputed in TMEM by three passes of the fused kernel
+  bool fused_dist = false;
+  if (!fused && a.Ps > 1 && mode != C3D_MODE_F32 && dt == kBF16) {
+    DevBuf mx(static_cast<size_t>(srows) * sizeof(float), s);
+    DevBuf sm(static_cast<size_t>(srows) * sizeof(float), s);
+    DevBuf partial(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+    const View kv = qkv_view(qkv.data, dt, a, 1, false), vv = qkv_view(qkv.data, dt, a, 2, true);
+    const View pv = scores_view(pb.get(), dt, a, false), cv = packed_out(partial.get(), dt, a, true);
+    if (attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 1,
+                       mx.as<float>(), sm.as<float>())) {
+      cube.all_reduce(a.seq_axis, mx.get(), srows, kF32, true, s);
+      attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 2,
+                     mx.as<float>(), sm.as<float>());
+      cube.all_reduce(a.seq_axis, sm.get(), srows, kF32, false, s);
+      attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 3,
+                     mx.as<float>(), sm.as<float>());
+      cube.reduce_scatter(a.seq_axis, partial.get(), ctx.data, rows * a.hd, dt, s);
+      cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+      fused_dist = true;
+    }
+  }
+  if (!fused && !fused_dist) {
     DevBuf sc(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
     e.out = scores_view(sc.get(), kF32, a, false);
@@ -381,7 +404,7 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
     }
   }
   // context = P V, reduce-scattered back to this rank's seq block
-  if (!fused) {
+  if (!fused && !fused_dist) {
     Epilogue e;
     DevBuf partial;
     if (a.Ps == 1) {

@@ -21,9 +21,13 @@ void prof_read_comm(double* ms, double* bytes, long long* calls);
 // Fused attention core (attention.cu) for slices holding the whole key range: scores
 // in TMEM, softmax, probabilities saved to `probs`, context = P V into `ctx`. Returns
 // false (nothing launched) when the shapes are outside its limits.
+// mode 0: whole softmax locally; modes 1-3: distributed softmax over a split key range
+// (1 local row max -> stat_max, 2 row sum with the all-reduced max -> stat_sum, 3 P and
+// the partial context with both all-reduced).
 bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
                     int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
-                    cudaStream_t s);
+                    cudaStream_t s, int mode = 0, float* stat_max = nullptr,
+                    float* stat_sum = nullptr);
 
 // Fused attention backward core (attention.cu) for the same case: dP in TMEM, dS =
 // P * (dP - rowdot) * scale written to `ds` and used in shared memory for dQ = dS K.

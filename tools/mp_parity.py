@@ -173,6 +173,42 @@ def layer_check(cube, dims, name, dtype, mode):
     report(f"layer-{name}-traffic-balanced", sent == recv, f"sent={sent} recv={recv}")
 
 
+def layer_tc_check(cube, dims):
+    """bf16 layer at a shape that takes the fused tcgen05 attention kernels (dh = 64,
+    256 / 512 keys per rank; with the seq axis split, the distributed-softmax passes)
+    against the fp64 oracle on the same bf16-rounded inputs."""
+    b, s, n, h = 2, 512, 8, 512
+    P = O.init_layer_params(h, 41)
+    gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
+    r = O.Rng(42)
+    x = bf16_round(O.random_matrix(b * s, h, r))
+    dy = bf16_round(O.random_matrix(b * s, h, r))
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params = c3.partition_layer_params(cube, gp, 0, c3.BF16)
+    X = c3.activation_to_device(cube, x, b, s, 0, c3.BF16)
+    DY = c3.activation_to_device(cube, dy, b, s, 0, c3.BF16)
+    y, saved = c3.transformer_layer_fwd(cube, X, params, cfg, c3.GroupState(0))
+    dx, grads = c3.transformer_layer_bwd(cube, DY, saved, params, cfg, grad_dtype=c3.F32)
+    torch.cuda.synchronize()
+    Y = c3.activation_to_global(gather_all(to_np(y.local)), b, s, h, 0, dims)
+    DX = c3.activation_to_global(gather_all(to_np(dx.local)), b, s, h, 0, dims)
+    PO = O.LayerParams(**{f: getattr(gp, f) for f in O.FIELDS})
+    yo, cache = O.layer_fwd(x, PO, b, s, n)
+    dxo, Go = O.layer_bwd(dy, cache, PO, b, s, n)
+    errs = {"y": O.normwise_err(Y, yo), "dx": O.normwise_err(DX, dxo)}
+    for f in O.FIELDS:
+        v = getattr(grads, f)
+        fam = gather_all(to_np(v.shard))
+        if f.startswith("w_"):
+            G = c3.collect(fam, c3.WEIGHT, dims, v.global_rows, v.global_cols, v.dirs)
+        else:
+            G = c3.collect_diagonal(fam, dims, v.global_len)
+        errs[f] = O.normwise_err(G, getattr(Go, f).reshape(G.shape))
+    worst = max(errs, key=errs.get)
+    report("layer-bf16-fused-attention-shape", all(e < 2e-2 for e in errs.values()),
+           f"worst {worst}={errs[worst]:.2e}")
+
+
 def loss_check(cube, dims):
     """3-D cross-entropy on the grid vs the (finite-difference-checked) oracle."""
     q = dims[0] * dims[1] * dims[2]
@@ -212,6 +248,7 @@ def main():
         matmul_checks(cube, dims)
     if dims[1] == dims[2]:
         loss_check(cube, dims)
+        layer_tc_check(cube, dims)
         for name in ("layer_toy", "layer_small"):
             layer_check(cube, dims, name, c3.F32, c3.MODE_F32)
             layer_check(cube, dims, name, c3.BF16, c3.MODE_AUTO)
