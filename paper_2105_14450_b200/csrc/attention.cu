@@ -288,9 +288,11 @@ void launch_attn(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& 
 struct AttnBwdArgs {
   int S, keys, H;
   float scale;
-  const float* rowdot;  // D per (slice, query)
-  __nv_bfloat16* dq;
-  long long dq_sr, dq_sb_lo, dq_sb_hi;
+  int o_split;          // rows per gathered dO block (0: not split)
+  const float* rowdot;  // D per (slice, query): [slice][S], or [S / rd_split][slices][rd_split]
+  long long rd_split, rd_slices;
+  __nv_bfloat16* dq;    // dQ, or its partial [p][rows][hd] when the seq axis is split
+  long long dq_sr, dq_sb_lo, dq_sb_hi, dq_split, dq_s_hi;
 };
 
 template <int KEYS>
@@ -337,7 +339,8 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
   if (warp == 0) {
     if (lane == 0) {
       ptx::mbar_arrive_expect_tx(bar_a, kOBytes + kVBytes);
-      ptx::tma_load_5d(sO, &tmDO, bar_a, 0, q0, 0, c3, c4);
+      ptx::tma_load_5d(sO, &tmDO, bar_a, 0, args.o_split ? q0 % args.o_split : q0,
+                       args.o_split ? q0 / args.o_split : 0, c3, c4);
 #pragma unroll
       for (int h = 0; h < KEYS / 256; ++h)
         ptx::tma_load_5d(sV + h * 256 * 128, &tmV, bar_a, 0, h * 256, 0, c3, c4);
@@ -385,7 +388,11 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
     const int row = quarter * 32 + lane;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const int c0 = group * kGroupCols;
-    const float sd = args.scale * __ldg(args.rowdot + static_cast<long long>(b) * args.S + q0 + row);
+    const long long q = q0 + row;
+    const long long ri = args.rd_split ? (q / args.rd_split) * (args.rd_slices * args.rd_split) +
+                                             b * args.rd_split + q % args.rd_split
+                                       : static_cast<long long>(b) * args.S + q;
+    const float sd = args.scale * __ldg(args.rowdot + ri);
     ptx::mbar_wait(bar_p, 0);
     ptx::mbar_wait(bar_s, 0);
     ptx::tc_fence_after();
@@ -425,8 +432,10 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
       ptx::tc_fence_after();
       float o[32];
       ptx::tmem_ld32(trow + group * 32, o);
-      __nv_bfloat16* dst = args.dq + c3 * args.dq_sb_lo + c4 * args.dq_sb_hi +
-                           static_cast<long long>(q0 + row) * args.dq_sr + group * 32;
+      const long long qoff = args.dq_split ? (q % args.dq_split) * args.dq_sr +
+                                                 (q / args.dq_split) * args.dq_s_hi
+                                           : q * args.dq_sr;
+      __nv_bfloat16* dst = args.dq + c3 * args.dq_sb_lo + c4 * args.dq_sb_hi + qoff + group * 32;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 pk;
@@ -523,14 +532,19 @@ namespace c3d {
 
 bool attn_bwd_fused(const View& d_o, const View& v, const View& k_mn, const View& probs,
                     const View& ds, const View& dq, const float* rowdot, int64_t S, int64_t keys,
-                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s) {
+                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s,
+                    int64_t rd_split) {
   if (std::getenv("C3D_NO_FUSED_ATTN") || std::getenv("C3D_NO_FUSED_ATTN_BWD")) return false;
   if (dh != kDh || S % kQ || (keys != 256 && keys != 512) || H <= 0 || !rowdot) return false;
   for (const View* w : {&d_o, &v, &k_mn, &probs, &ds, &dq}) {
     if (w->dtype != kBF16 || reinterpret_cast<uintptr_t>(w->base) % 16) return false;
-    if (w->rsplit || w->csplit || w->b_lo_n != H) return false;
+    if (w->csplit || w->b_lo_n != H) return false;
   }
-  if (dq.sc != 1 || (dq.sr * 2) % 16 || (dq.sb_lo * 2) % 16 || (dq.sb_hi * 2) % 16) return false;
+  if (v.rsplit || k_mn.rsplit || probs.rsplit || ds.rsplit) return false;
+  if ((d_o.rsplit && d_o.rsplit % kQ) || (dq.rsplit && dq.rsplit % kQ)) return false;
+  if (dq.sc != 1 || (dq.sr * 2) % 16 || (dq.sb_lo * 2) % 16 || (dq.sb_hi * 2) % 16 ||
+      (dq.s_hi * 2) % 16)
+    return false;
   int mn = 0;
   const CUtensorMap mo = tc_operand_map(d_o, S, dh, nslices, kQ, &mn);
   if (mn) return false;
@@ -546,11 +560,16 @@ bool attn_bwd_fused(const View& d_o, const View& v, const View& k_mn, const View
   a.keys = static_cast<int>(keys);
   a.H = static_cast<int>(H);
   a.scale = scale;
+  a.o_split = static_cast<int>(d_o.rsplit);
   a.rowdot = rowdot;
+  a.rd_split = rd_split;
+  a.rd_slices = nslices;
   a.dq = static_cast<__nv_bfloat16*>(dq.base);
   a.dq_sr = dq.sr;
   a.dq_sb_lo = dq.sb_lo;
   a.dq_sb_hi = dq.sb_hi;
+  a.dq_split = dq.rsplit;
+  a.dq_s_hi = dq.s_hi;
   if (keys == 512) launch_attn_bwd<512>(mo, mv, mk, mp, mds, a, nslices, s);
   else launch_attn_bwd<256>(mo, mv, mk, mp, mds, a, nslices, s);
   check_launch("attn_bwd_fused");

@@ -450,6 +450,27 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                         !std::getenv("C3D_NO_FUSED_ATTN");
   DevBuf dpf;
   bool fused_dq = false;  // dS and dQ from the fused attention-backward kernel
+  DevBuf dq_partial;      // split seq axis: the fused kernel's partial dQ, reduce-scattered
+  if (a.Ps > 1 && mode != C3D_MODE_F32 && dt == kBF16 && !std::getenv("C3D_NO_FUSED_ATTN")) {
+    // D = rowsum(dctx * ctx) on this rank's query rows, all-gathered along the seq axis
+    DevBuf rdl(static_cast<size_t>(nslices * a.sl) * sizeof(float), s);
+    k_attn_rowdot(dctx.data, S.out_lin.x.data, dt, nslices, a.sl, a.H, a.dh, a.sl * a.hd,
+                  rdl.as<float>(), s);
+    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
+    cube.all_gather(a.seq_axis, rdl.get(), rd.get(), static_cast<size_t>(nslices * a.sl), kF32, s);
+    dq_partial = DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+    fused_dq = attn_bwd_fused(packed_view(dcf.ptr, dt, a, false), qkv_view(qkv, dt, a, 2, false),
+                              qkv_view(qkv, dt, a, 1, true), scores_view(S.probs, dt, a, false),
+                              scores_view(dp.get(), dt, a, false),
+                              packed_out(dq_partial.get(), dt, a, true), rd.as<float>(), a.S,
+                              a.sl, a.dh, a.H, nslices, a.scale, s, a.sl);
+    if (fused_dq) {
+      cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+      DevBuf dq(static_cast<size_t>(rows * a.hd) * dtype_size(dt), s);
+      cube.reduce_scatter(a.seq_axis, dq_partial.get(), dq.get(), rows * a.hd, dt, s);
+      k_copy_heads(dq.get(), a.hd, a.dh, dqkv_buf.get(), a.ld_qkv, 3 * a.dh, rows, a.H, a.dh, dt, s);
+    }
+  }
   if (fused_ds) {
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
     k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
@@ -475,7 +496,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
     e.rv_div = a.sl;
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
                qkv_view(qkv, dt, a, 2, false), e, s);
-  } else if (!fused_ds) {
+  } else if (!fused_ds && !fused_dq) {
     // dP = dctx_full V^T (fp32)
     dpf = DevBuf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
@@ -491,7 +512,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                packed_view(dcf.ptr, dt, a, true), e, s);
   }
   // dS = P * (dP - rowdot) * scale, rowdot summed along the seq axis
-  if (fused_ds) {
+  if (fused_ds || fused_dq) {
   } else if (a.Ps == 1) {
     k_softmax_bwd_fused(dpf.as<float>(), S.probs, dt, srows, a.sl, a.scale, dp.get(), dt, s);
   } else {

@@ -31,9 +31,12 @@ bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& pro
 
 // Fused attention backward core (attention.cu) for the same case: dP in TMEM, dS =
 // P * (dP - rowdot) * scale written to `ds` and used in shared memory for dQ = dS K.
+// `rd_split` > 0: rowdot is laid out [S / rd_split][slices][rd_split] (all-gathered along
+// the seq axis); d_o and dq may be row-split (gathered dO, partial dQ).
 bool attn_bwd_fused(const View& d_o, const View& v, const View& k_mn, const View& probs,
                     const View& ds, const View& dq, const float* rowdot, int64_t S, int64_t keys,
-                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s);
+                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s,
+                    int64_t rd_split = 0);
 
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
