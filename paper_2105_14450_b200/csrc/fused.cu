@@ -63,7 +63,6 @@ struct FinishArgs {
   long long rows, cols;
   int dtype;
   int vec;
-  uint32_t* reset;  // gathered-operand ready flag consumed by the GEMM (cleared here)
   Epilogue e;  // out = contiguous [rows][cols]
 };
 
@@ -113,7 +112,6 @@ __global__ void __launch_bounds__(256) rs_finish_kernel(const FinishArgs a) {
     ptx::wait_epoch(a.done[k] + a.done_offset + cta, epoch);
   }
   __syncthreads();
-  if (a.reset && blockIdx.x == 0 && threadIdx.x == 0) *a.reset = 0u;
   const Epilogue& e = a.e;
   constexpr long long es = DT == kF32 ? 4 : 2;
   const long long total = a.rows * a.cols;
@@ -176,7 +174,7 @@ __global__ void __launch_bounds__(256) rs_finish_kernel(const FinishArgs a) {
 
 void launch_finish(Cube& cube, SymmHeap* h, int axis, int grid, int done_offset,
                    const char* slots, long long slot_elems, long long rows, long long cols,
-                   const Epilogue& post, cudaStream_t s, uint32_t* reset = nullptr) {
+                   const Epilogue& post, cudaStream_t s) {
   const int P = cube.extent(axis);
   const std::vector<int>& line = cube.line(axis);
   FinishArgs fa{};
@@ -193,7 +191,6 @@ void launch_finish(Cube& cube, SymmHeap* h, int axis, int grid, int done_offset,
   fa.cols = cols;
   const int dtype = post.out.dtype;
   fa.dtype = dtype;
-  fa.reset = reset;
   fa.e = post;
   auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
   bool vec = cols % 8 == 0 && al(post.out.base) && post.out.sr == cols && post.alpha == 1.f &&

@@ -8,8 +8,11 @@
 // Structure (one CTA per SM, persistent over work units = output tiles x K splits):
 //   warp 0      TMA producer (one lane)                  smem ring: full/empty mbarriers
 //   warp 1      TMEM allocator + UMMA issuer (one lane)  TMEM ring: 2 accumulators
-//   warps 2..9  epilogue: tcgen05.ld -> registers -> epilogue math -> st.global
-//               (two warps per TMEM lane quarter, each owning half of the columns)
+//   warps 2..9  epilogue: tcgen05.ld (32-column halves) -> registers -> epilogue math ->
+//               128B-swizzled smem staging -> TMA bulk-tensor store (two warps per
+//               TMEM lane quarter, each owning half of the columns); aux operands
+//               arrive by TMA into a second per-warp buffer; row-wise st.global
+//               fallback when the output view is not TMA-addressable
 // Tile: 128 x BN (UMMA M=128, N=BN, K=16), K-block 64 per pipeline stage. The
 // producer and issuer loops carry their stage/phase and TMA coordinates
 // incrementally: no integer division on the per-K-block path.
@@ -79,33 +82,6 @@ struct TcArgs {
 struct RsMaps {
   CUtensorMap m[kRsMax];
 };
-
-// Writes one 32-value row segment (CW = 32 fp32 or 64 bf16 values = 128 B) into row
-// `lane` of a [32][128 B] tile laid out with the TMA 128B swizzle (16-B chunk j of row
-// r lives at chunk j ^ (r & 7)); conflict-free for a warp writing one row per lane.
-template <int CW>
-__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float* v) {
-  uint8_t* row = buf + lane * 128;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint8_t* dst = row + ((j ^ (lane & 7)) << 4);
-    if (CW == 32) {
-      *reinterpret_cast<float4*>(dst) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    } else {
-      uint4 pk;
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
-      __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
-      __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
-      pk.x = *reinterpret_cast<uint32_t*>(&h0);
-      pk.y = *reinterpret_cast<uint32_t*>(&h1);
-      pk.z = *reinterpret_cast<uint32_t*>(&h2);
-      pk.w = *reinterpret_cast<uint32_t*>(&h3);
-      *reinterpret_cast<uint4*>(dst) = pk;
-    }
-  }
-}
 
 // Writes one 16-B chunk j (8 bf16 or 4 fp32 values) of row `lane` of the swizzled
 // staging tile.
@@ -318,26 +294,6 @@ __device__ __forceinline__ void epilogue_row32(const TcArgs& args, long long off
     for (int j = 0; j < 32; ++j)
       if (j < nvalid) epi_scalar(e, off + j, n0 + j, v[j]);
   }
-}
-
-// One 16-B raw chunk holds 8 bf16 or 4 fp32 values; element j of a CW-wide row segment
-// (CW = 64 bf16 or 32 fp32: 8 chunks either way).
-template <int CW>
-__device__ __forceinline__ float raw_at(const uint4 (&raw)[8], int j) {
-  if (CW == 32) {
-    return __uint_as_float(reinterpret_cast<const uint32_t*>(&raw[j >> 2])[j & 3]);
-  } else {
-    const uint32_t w = reinterpret_cast<const uint32_t*>(&raw[j >> 3])[(j & 7) >> 1];
-    return __uint_as_float((j & 1) ? (w & 0xFFFF0000u) : (w << 16));
-  }
-}
-
-template <int CW>
-__device__ __forceinline__ void load_raw(const void* base, int dtype, long long off, uint4 (&raw)[8]) {
-  const uint4* p = reinterpret_cast<const uint4*>(static_cast<const char*>(base) +
-                                                  off * (dtype == kF32 ? 4 : 2));
-#pragma unroll
-  for (int q = 0; q < 8; ++q) raw[q] = __ldg(p + q);
 }
 
 // Element j (0..CW) of row `lane` of a swizzled [32][128 B] chunk buffer.
