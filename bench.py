@@ -510,6 +510,11 @@ def our_arm(args, wl):
             "collectives": {"calls_per_step": comm_n / prof_steps,
                             "ms_per_step": comm_ms / prof_steps,
                             "payload_mb_per_step": comm_bytes / prof_steps / 1e6,
+                            # axis lines have 2 ranks here: (p - 1) / p of each payload
+                            # crosses NVLink per rank
+                            "nvlink_bus_gbs": (comm_bytes * 0.5 / (comm_ms * 1e-3) / 1e9
+                                               if comm_ms > 0 else None),
+                            "fused_gemm_reduce_scatter": "not included (inside the GEMMs)",
                             "timing": f"per-call CUDA events on the issuing stream, rank 0, "
                                       f"{prof_src}"},
             "clocks": clk,
