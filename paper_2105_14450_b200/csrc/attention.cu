@@ -188,7 +188,12 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
         float v[32];
         ptx::tmem_ld32(trow + c, v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) sum += exp2f(fmaf(v[j], args.scale_log2, -ms));
+        for (int j = 0; j < 32; ++j) {
+          v[j] = exp2f(fmaf(v[j], args.scale_log2, -ms));
+          sum += v[j];
+        }
+        // keep exp(s - m) in TMEM: the normalising pass only scales it
+        if (MODE == 0) ptx::tmem_st32(trow + c, v);
       }
       red[4 * kQ + group * kQ + row] = sum;
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kSoftWarps) : "memory");
@@ -201,18 +206,18 @@ __global__ void __launch_bounds__(kThreadsAttn, 1)
     for (int c = c0; c < c0 + kGroupCols; c += 32) {
       float v[32];
       ptx::tmem_ld32(trow + c, v);
+      if (MODE != 0) {  // mode 0 left exp(s - m) in TMEM
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = exp2f(fmaf(v[j], args.scale_log2, -ms));
+      }
       uint8_t* chunk_row = sP + (c >> 6) * 16384 + row * 128;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 pk;
-        pk.x = pack_bf16(exp2f(fmaf(v[8 * j + 0], args.scale_log2, -ms)) * inv,
-                         exp2f(fmaf(v[8 * j + 1], args.scale_log2, -ms)) * inv);
-        pk.y = pack_bf16(exp2f(fmaf(v[8 * j + 2], args.scale_log2, -ms)) * inv,
-                         exp2f(fmaf(v[8 * j + 3], args.scale_log2, -ms)) * inv);
-        pk.z = pack_bf16(exp2f(fmaf(v[8 * j + 4], args.scale_log2, -ms)) * inv,
-                         exp2f(fmaf(v[8 * j + 5], args.scale_log2, -ms)) * inv);
-        pk.w = pack_bf16(exp2f(fmaf(v[8 * j + 6], args.scale_log2, -ms)) * inv,
-                         exp2f(fmaf(v[8 * j + 7], args.scale_log2, -ms)) * inv);
+        pk.x = pack_bf16(v[8 * j + 0] * inv, v[8 * j + 1] * inv);
+        pk.y = pack_bf16(v[8 * j + 2] * inv, v[8 * j + 3] * inv);
+        pk.z = pack_bf16(v[8 * j + 4] * inv, v[8 * j + 5] * inv);
+        pk.w = pack_bf16(v[8 * j + 6] * inv, v[8 * j + 7] * inv);
         const int chunk = ((c >> 5) & 1) * 4 + j;
         *reinterpret_cast<uint4*>(chunk_row + ((chunk ^ (row & 7)) << 4)) = pk;
       }
