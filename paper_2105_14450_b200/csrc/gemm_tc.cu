@@ -56,6 +56,7 @@ struct TcOperand {
 struct TcArgs {
   int M, N, K, batch;
   int m_tiles, n_tiles, k_blocks;
+  int group_m;  // tile rows per rasterisation band (1: plain m-major order)
   int num_tiles;  // output tiles (batch * m_tiles * n_tiles)
   int ksplit, kb_per_split;
   int stages;
@@ -175,9 +176,17 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
   const int per_batch = a.m_tiles * a.n_tiles;
   u.b = tile / per_batch;
   const int rem = tile - u.b * per_batch;
-  const int mt = rem / a.n_tiles;
+  // grouped rasterisation: a wave of CTAs covers a group_m-row band of tiles, so the A
+  // and B panels of one wave stay resident in L2 even when B alone is larger than L2
+  // (m-major order re-streams all of B for every tile row: 442 GB at M=N=K=32768)
+  const int group = rem / (a.group_m * a.n_tiles);
+  const int first_m = group * a.group_m;
+  const int gsize = min(a.m_tiles - first_m, a.group_m);
+  const int within = rem - group * (a.group_m * a.n_tiles);
+  const int nt = within / gsize;
+  const int mt = first_m + (within - nt * gsize);
   u.m0 = mt * kBM;
-  u.n0 = (rem - mt * a.n_tiles) * bn;
+  u.n0 = nt * bn;
   u.kb0 = u.ks * a.kb_per_split;
   u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
   return u;
@@ -1042,6 +1051,9 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.n_tiles = static_cast<int>((p.N + bn - 1) / bn);
   args.k_blocks = static_cast<int>((p.K + kBK - 1) / kBK);
   args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
+  // bands of 16 tile rows once the B operand outgrows a comfortable share of L2
+  args.group_m = (p.N * p.K * 2 > (48ll << 20)) ? std::min(16, args.m_tiles) : 1;
+  if (const char* e = std::getenv("C3D_GROUP_M")) args.group_m = std::max(1, std::min(std::atoi(e), args.m_tiles));
   args.ksplit = p.rs.P > 1 ? 1
                             : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms);
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
