@@ -468,10 +468,24 @@ def our_arm(args, wl):
         except Exception:
             traffic = None
     # layer-level algorithmic flops (reference cost model, cube3d/cost_model.hpp:195-208)
-    from oracle.cube3d_oracle import layer_madds
-    mf, mb = layer_madds(b, s, n, h, 1)
-    layer_flops = 2.0 * (mf + mb)
+    # algorithmic work of one step from the library's own CostCounters (charged with the
+    # reference's cost model, cube3d/cost_model.hpp:183-208): multiply-adds summed over
+    # ranks, elements sent per rank (max over ranks)
+    cube.reset_counters()
+    step(x, dy)
+    torch.cuda.synchronize()
+    cnt = cube.counters()
+    layer_flops = 2.0 * dist.sum_over_ranks(float(cnt["multiply_adds"]))
+    sent = dist.max_over_ranks(float(cnt["elements_sent"]))
     layer_tflops = layer_flops / (ms_max * 1e-3) / 1e12
+    nvlink_gbs = 770.0  # measured peer bandwidth per direction (B200_PROFILING.md)
+    bound = {"flop_ms": layer_flops / (peak_tc * 1e12 * world) * 1e3,
+             "comm_ms": sent * 2 / (nvlink_gbs * 1e9) * 1e3}
+    layer_roofline = {**bound, "bound_ms": max(bound.values()),
+                      "frac": max(bound.values()) / ms_max,
+                      "elements_sent_per_rank": sent,
+                      "note": "max(flops / (sustained bf16 peak x GPUs), elements sent per rank "
+                              "x 2 B / 770 GB/s) / measured ms; HBM-bound kernels not included"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -508,6 +522,7 @@ def our_arm(args, wl):
             "layer_tflops": layer_tflops,
             "matmul": mm,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
+            "layer_roofline": layer_roofline,
             "collectives": {"calls_per_step": comm_n / prof_steps,
                             "ms_per_step": comm_ms / prof_steps,
                             "payload_mb_per_step": comm_bytes / prof_steps / 1e6,
