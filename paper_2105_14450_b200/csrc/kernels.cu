@@ -436,6 +436,56 @@ __global__ void ln_bwd_rows_vec_kernel(const void* dy, int dt, const void* xhat,
   }
 }
 
+// Local row moments over this rank's column block: st[2r] = mean, st[2r+1] = centred
+// sum of squares (Chan et al.'s pairwise combination then merges the blocks exactly).
+template <int VPL>
+__global__ void row_moments_vec_kernel(const void* x, int dt, int64_t rows, float* st) {
+  constexpr int64_t cols = 256 * VPL;
+  const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (r >= rows) return;
+  float v[VPL][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    vload8(x, dt, r * cols + (k * 32 + lane) * 8, v[k]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[k][i];
+  }
+  const float mean = warp_sum(s) * (1.f / static_cast<float>(cols));
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float d = v[k][i] - mean;
+      q += d * d;
+    }
+  q = warp_sum(q);
+  if (lane == 0) {
+    st[2 * r] = mean;
+    st[2 * r + 1] = q;
+  }
+}
+
+// Merges the P gathered (mean, M2) pairs of each row (equal block sizes n) into the
+// full-row sum and centred sum of squares.
+__global__ void combine_moments_kernel(const float* st, int P, int64_t rows, float n,
+                                       float* sums, float* sq) {
+  const int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (r >= rows) return;
+  float m = 0.f;
+  for (int p = 0; p < P; ++p) m += st[p * 2 * rows + 2 * r];
+  m /= static_cast<float>(P);
+  float q = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float d = st[p * 2 * rows + 2 * r] - m;
+    q += st[p * 2 * rows + 2 * r + 1] + n * d * d;
+  }
+  sums[r] = m * n * static_cast<float>(P);
+  sq[r] = q;
+}
+
 // Row statistics and dx in one pass when they need no all-reduce (p_out = 1):
 // g = dy * gamma, s = sum g, d = sum g * xhat, dx = inv_std * (g - s/h - xhat * d/h) (+ resid).
 // With `grs` the row sums come all-reduced ([s | d], scaled by ginv_h).
@@ -587,6 +637,26 @@ void by_vpl(int vpl, F&& f) {
   else f(std::integral_constant<int, 8>{});
 }
 }  // namespace
+
+bool k_row_moments(const void* x, int dt, int64_t rows, int64_t cols, float* st, cudaStream_t s) {
+  const int vpl = ln_vpl(cols);
+  if (!vpl || !al16(x)) return false;
+  if (rows == 0) return true;
+  by_vpl(vpl, [&](auto V) {
+    row_moments_vec_kernel<decltype(V)::value><<<row_blocks(rows), 32 * kWarpsPerBlock, 0, s>>>(
+        x, dt, rows, st);
+  });
+  check_launch("row_moments");
+  return true;
+}
+
+void k_combine_moments(const float* st, int P, int64_t rows, int64_t n, float* sums, float* sq,
+                       cudaStream_t s) {
+  if (rows == 0) return;
+  combine_moments_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(
+      st, P, rows, static_cast<float>(n), sums, sq);
+  check_launch("combine_moments");
+}
 
 void k_row_sum(const void* x, int dt, int64_t rows, int64_t cols, const float* sums,
                float inv_h, float* out, cudaStream_t s) {

@@ -44,6 +44,12 @@ void k_ln_fwd_fused(const void* x, int dt, int64_t rows, int64_t cols, float eps
                     const float* gamma, const float* beta, void* y, int ydt, void* xhat,
                     int xhdt, float* inv_std, cudaStream_t s);
 // row_sum[r] = sum_c dy*gamma, row_dot[r] = sum_c dy*gamma*xhat (into rs[0:rows], rs[rows:2rows]).
+// Distributed LayerNorm statistics in one collective: local (mean, M2) per row, gathered
+// along the output axis ([P][rows][2]) and merged (Chan et al.) into sums / centred sum of
+// squares for k_ln_apply. k_row_moments returns false without a vectorised form.
+bool k_row_moments(const void* x, int dt, int64_t rows, int64_t cols, float* st, cudaStream_t s);
+void k_combine_moments(const float* st, int P, int64_t rows, int64_t n, float* sums, float* sq,
+                       cudaStream_t s);
 // p_out = 1 backward in one pass (row sums and dx); false when the shape has no
 // vectorised form (the caller then runs k_ln_bwd_rows + k_ln_bwd_dx).
 bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,

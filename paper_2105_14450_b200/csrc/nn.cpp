@@ -182,10 +182,18 @@ void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, 
   } else {
     DevBuf sums(static_cast<size_t>(x.rows) * sizeof(float), s);
     DevBuf sq(static_cast<size_t>(x.rows) * sizeof(float), s);
-    k_row_sum(x.data, x.dtype, x.rows, x.cols, nullptr, inv_h, sums.as<float>(), s);
-    cube.all_reduce(d.out, sums.get(), x.rows, kF32, false, s);
-    k_row_sum(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), inv_h, sq.as<float>(), s);
-    cube.all_reduce(d.out, sq.get(), x.rows, kF32, false, s);
+    DevBuf st(static_cast<size_t>(2 * x.rows) * sizeof(float), s);
+    if (k_row_moments(x.data, x.dtype, x.rows, x.cols, st.as<float>(), s)) {
+      // one all-gather of per-block (mean, M2) instead of two all-reduces (same elements)
+      DevBuf all(static_cast<size_t>(2 * x.rows * Pout) * sizeof(float), s);
+      cube.all_gather(d.out, st.get(), all.get(), static_cast<size_t>(2 * x.rows), kF32, s);
+      k_combine_moments(all.as<float>(), Pout, x.rows, x.cols, sums.as<float>(), sq.as<float>(), s);
+    } else {
+      k_row_sum(x.data, x.dtype, x.rows, x.cols, nullptr, inv_h, sums.as<float>(), s);
+      cube.all_reduce(d.out, sums.get(), x.rows, kF32, false, s);
+      k_row_sum(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), inv_h, sq.as<float>(), s);
+      cube.all_reduce(d.out, sq.get(), x.rows, kF32, false, s);
+    }
     k_ln_apply(x.data, x.dtype, x.rows, x.cols, sums.as<float>(), sq.as<float>(), inv_h,
                static_cast<float>(eps), gb, bb, y.data, y.dtype, xhat.get(), x.dtype,
                inv_std.as<float>(), s);
