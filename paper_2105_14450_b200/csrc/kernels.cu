@@ -187,6 +187,26 @@ __global__ void colsum_partial_vec_kernel(const void* x, const void* y, int64_t 
   reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
 }
 
+// Second stage over many chunks: 8 warps split the chunks of 32 columns, partials merged
+// in a fixed order through shared memory (deterministic).
+__global__ void colsum_final_wide_kernel(const float* partial, int64_t chunks, int64_t cols,
+                                         float* out) {
+  __shared__ float red[8][32];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int64_t c = blockIdx.x * 32LL + lane;
+  float acc = 0.f;
+  if (c < cols)
+    for (int64_t k = w; k < chunks; k += 8) acc += partial[k * cols + c];
+  red[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    out[c] = t;
+  }
+}
+
 __global__ void colsum_final_kernel(const float* partial, int64_t chunks, int64_t cols,
                                     float* out) {
   const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -595,8 +615,12 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
     }
     check_launch("colsum_partial");
   }
-  colsum_final_kernel<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, s>>>(partial, chunks,
-                                                                                cols, out);
+  if (chunks >= 32)
+    colsum_final_wide_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(partial, chunks,
+                                                                                   cols, out);
+  else
+    colsum_final_kernel<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, s>>>(partial, chunks,
+                                                                                  cols, out);
   check_launch("colsum_final");
   C3D_CUDA(cudaFreeAsync(partial, s));
 }
