@@ -510,7 +510,7 @@ __global__ void combine_moments_kernel(const float* st, int P, int64_t rows, flo
 // g = dy * gamma, s = sum g, d = sum g * xhat, dx = inv_std * (g - s/h - xhat * d/h) (+ resid).
 // With `grs` the row sums come all-reduced ([s | d], scaled by ginv_h).
 template <int VPL>
-__global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int xdt,
+__global__ void __launch_bounds__(256, 2) ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int xdt,
                                   const float* gamma, const float* inv_std, int64_t rows,
                                   const void* resid, int rdt, void* dx, int dxdt,
                                   const float* grs, float ginv_h) {
@@ -518,12 +518,8 @@ __global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int 
   const int64_t r = blockIdx.x * static_cast<int64_t>(kWarpsPerBlock) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (r >= rows) return;
-  float g[VPL][8], xh[VPL][8], rr[VPL][8];
+  float g[VPL][8], xh[VPL][8];
   float s = 0.f, d = 0.f;
-  if (resid) {  // issued with the other loads, consumed after the row reductions
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) vload8(resid, rdt, r * cols + (k * 32 + lane) * 8, rr[k]);
-  }
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const int64_t c = (k * 32 + lane) * 8;
@@ -551,11 +547,12 @@ __global__ void ln_bwd_vec_kernel(const void* dy, int dt, const void* xhat, int 
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const int64_t c = (k * 32 + lane) * 8;
-    float o[8];
+    float o[8], rr[8];
+    if (resid) vload8(resid, rdt, r * cols + c, rr);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       o[i] = inv * (g[k][i] - s - xh[k][i] * d);
-      if (resid) o[i] += rr[k][i];
+      if (resid) o[i] += rr[i];
     }
     vstore8(dx, dxdt, r * cols + c, o);
   }
