@@ -116,3 +116,14 @@ def test_simt_matches(torch_cuda):
     torch = torch_cuda
     got, ref = _run(torch, 96, 80, 40, False, True, mode=c3.MODE_F32)
     assert (got - ref).abs().max().item() < 1e-4
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True)])
+def test_grouped_rasterisation_large_b(torch_cuda, a_mn, b_mn):
+    """B larger than the grouping threshold (48 MB) switches to 16-row tile bands; with
+    20 tile rows (one full band + a partial one) every output tile must be produced once
+    (integer inputs: bitwise)."""
+    torch = torch_cuda
+    got, ref = _run(torch, 128 * 20, 4096, 8192, a_mn, b_mn, integer=True)
+    assert not torch.isnan(got).any()
+    assert torch.equal(got, ref)
