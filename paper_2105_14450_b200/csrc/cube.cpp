@@ -65,19 +65,10 @@ Cube::Cube(const int dims[3], int rank, int device, const unsigned char* uid)
     }
   }
   for (int a = 0; a < 3; ++a) line_[a] = grid_.axis_group(coords_, a);
-  if (symm_) {
-    C3D_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
-    C3D_CUDA(cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming));
-    C3D_CUDA(cudaEventCreateWithFlags(&join_, cudaEventDisableTiming));
-  }
 }
 
 Cube::~Cube() {
-  if (side_) cudaStreamSynchronize(side_);
   symm_.reset();
-  if (fork_) cudaEventDestroy(fork_);
-  if (join_) cudaEventDestroy(join_);
-  if (side_) cudaStreamDestroy(side_);
   for (auto& c : axis_comm_)
     if (c) ncclCommDestroy(c);
   if (world_) ncclCommDestroy(world_);

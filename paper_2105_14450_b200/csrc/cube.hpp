@@ -90,10 +90,6 @@ class Cube {
   // Peer-memory transport, or null when collectives go through NCCL (C3D_NCCL_COLL=1).
   SymmHeap* symm() const { return symm_.get(); }
   const std::vector<int>& line(int axis) const { return line_[axis]; }
-  // Second stream (copy-engine pushes overlapping the main stream) and fork/join events.
-  cudaStream_t side_stream() const { return side_; }
-  cudaEvent_t fork_event() const { return fork_; }
-  cudaEvent_t join_event() const { return join_; }
 
   // Collectives along one axis line. Counts are in elements.
   void all_gather(int axis, const void* send, void* recv, size_t count, int dtype,
@@ -128,8 +124,6 @@ class Cube {
   ncclComm_t axis_comm_[3] = {nullptr, nullptr, nullptr};
   std::unique_ptr<SymmHeap> symm_;  // peer-memory transport (null: NCCL for everything)
   std::vector<int> line_[3];        // world ranks of this rank's axis lines, by position
-  cudaStream_t side_ = nullptr;
-  cudaEvent_t fork_ = nullptr, join_ = nullptr;
   c3d_counters counters_{};
 };
 
