@@ -207,7 +207,7 @@ template <int DT, bool VEC>
 void launch(const SymmArgs& a, cudaStream_t s) {
   static const int threads = [] {
     const char* e = std::getenv("C3D_SYMM_THREADS");
-    return e ? std::atoi(e) : 512;
+    return e ? std::atoi(e) : 1024;  // sweep (tools/symm_sweep.sh): 1024 x 1 per SM best
   }();
   symm_coll_kernel<DT, VEC><<<a.G, threads, 0, s>>>(a);
 }
@@ -352,7 +352,7 @@ void SymmHeap::all_gather_direct(const std::vector<int>& line, int pos, const vo
   }();
   static const int per_sm = [] {
     const char* e = std::getenv("C3D_SYMM_PER_SM");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 1;
   }();
   const size_t blocks = (count * es + chunk - 1) / chunk;
   a.G = static_cast<int>(std::max<size_t>(
@@ -413,7 +413,7 @@ void SymmHeap::collective(CollOp op, const std::vector<int>& line, int pos, cons
     }();
     static const int per_sm = [] {
       const char* e = std::getenv("C3D_SYMM_PER_SM");
-      return e ? std::atoi(e) : 2;
+      return e ? std::atoi(e) : 1;
     }();
     const size_t blocks = (n * es + chunk - 1) / chunk;
     a.G = static_cast<int>(std::max<size_t>(
