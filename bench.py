@@ -96,42 +96,55 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def measured_peaks():
+def measured_peaks(clk=None):
+    """(bf16 TFLOP/s peak, HBM GB/s peak, source). The bf16 denominator matches the clocks
+    the timed region ran at: the burst figure (measured at full SM clock) when the sampled
+    median SM clock is within 5% of its maximum, else the sustained one."""
     p = ROOT / "MEASURED_PEAKS.json"
-    if p.exists():
-        d = json.loads(p.read_text())
-        return d.get("bf16_tflops_sustained", 1400.2), d.get("hbm_gbs", 6552.3), "measured"
-    return 1400.0, 6650.0, "fallback"
+    d = json.loads(p.read_text()) if p.exists() else {}
+    burst = d.get("bf16_tflops", 1646.8)
+    sustained = d.get("bf16_tflops_sustained", 1400.2)
+    hbm = d.get("hbm_gbs", 6552.3)
+    src = "MEASURED_PEAKS.json" if d else "B200_PROFILING.md fallback"
+    full_clock = bool(clk and clk.get("sm_mhz") and clk.get("sm_max_mhz")
+                      and clk["sm_mhz"] >= 0.95 * clk["sm_max_mhz"])
+    if full_clock or not clk:
+        return burst, hbm, f"{src} bf16_tflops (burst; timed region at full SM clock)"
+    return sustained, hbm, f"{src} bf16_tflops_sustained (timed region below full SM clock)"
 
 
 # --------------------------------------------------------------- CPU reference
 def cpu_reference_sample(wl, p_ref=2, batch=2, seed=7):
-    """The reference's own CPU implementation (oracle/_ref: run_layer through its 3-D
-    path on a p=2 cube, one std::thread per rank) on a bounded batch of the workload.
-    Falls back to the numpy oracle port when the reference library was not built."""
+    """The reference's own CPU implementation (oracle/_ref: transformer_layer_fwd and
+    transformer_layer_bwd through its 3-D path on a p=2 cube, one std::thread per rank,
+    float) on a bounded batch of the workload; forward and backward timed separately
+    with an Endpoint barrier between them. Falls back to the numpy oracle port when the
+    reference library was not built. Returns (seconds, meta)."""
     import numpy as np
     from oracle import ref
     s, n, h = wl["s"], wl["n"], wl["h"]
     rng = np.random.default_rng(seed)
     x = rng.uniform(-1, 1, (batch * s, h))
     dy = rng.uniform(-1, 1, (batch * s, h))
+    nproc = os.cpu_count() or 1
     if ref.available():
         params = ref.init_layer_params(h, seed)
-        t0 = time.perf_counter()
-        ref.run_layer(p_ref, batch, s, n, h, params, x, dy, f32=True)
-        dt = time.perf_counter() - t0
-        return dt, dict(kind="reference", cores=p_ref ** 3,
-                        sample=f"reference run_layer<float> fwd+bwd, p={p_ref} cube "
-                               f"({p_ref ** 3} rank threads), batch {batch} of the "
-                               f"workload shape (s={s}, n={n}, h={h})")
+        tf, tb = ref.time_layer(p_ref, batch, s, n, h, params, x, dy)
+        return tf + tb, dict(kind="reference", cores=p_ref ** 3, host_nproc=nproc,
+                             fwd_s=tf, bwd_s=tb,
+                             sample=f"reference transformer_layer_fwd/bwd<float>, p={p_ref} cube "
+                                    f"({p_ref ** 3} rank threads = cores used), batch {batch} of "
+                                    f"the workload shape (s={s}, n={n}, h={h}); fwd and bwd timed "
+                                    f"separately (barrier between)")
     from oracle import cube3d_oracle as O
     P = O.init_layer_params(h, seed)
     t0 = time.perf_counter()
     y, c = O.layer_fwd(x, P, batch, s, n)
+    t1 = time.perf_counter()
     O.layer_bwd(dy, c, P, batch, s, n)
-    dt = time.perf_counter() - t0
-    return dt, dict(kind="port", cores=os.cpu_count() or 1,
-                    sample=f"numpy oracle port fwd+bwd, batch {batch} (s={s}, n={n}, h={h})")
+    t2 = time.perf_counter()
+    return t2 - t0, dict(kind="port", cores=nproc, host_nproc=nproc, fwd_s=t1 - t0, bwd_s=t2 - t1,
+                         sample=f"numpy oracle port fwd+bwd, batch {batch} (s={s}, n={n}, h={h})")
 
 
 def reference_arm(args, wl):
@@ -297,6 +310,38 @@ def e2e_pipelined(args, b, x, dy, step, stream, world):
                     "dx out, on two copy streams double-buffered against the compute"}
 
 
+# ------------------------------------------------------------ fp32-exact mode
+def fp32_mode_figure(cube, wl, steps=3):
+    """The same layer fwd+bwd in the fp32-exact mode (fp32 storage, SIMT fp32 GEMMs:
+    the oracle-comparison mode of the north star), device-resident, eager, CUDA events;
+    seq/s, max over ranks. A secondary figure: the headline is the bf16 mode."""
+    import torch
+    from paper_2105_14450_b200 import cube3d as c3
+    from paper_2105_14450_b200 import dist
+    b, s, n, h = wl["b"], wl["s"], wl["n"], wl["h"]
+    cfg = c3.TransformerConfig(b, s, n, h)
+    params, x, dy = make_layer_inputs(cube, wl, c3.F32)
+    grads = c3.empty_like_params(cube, params, c3.F32)
+
+    def step():
+        gs = c3.GroupState(0)
+        y, saved = c3.transformer_layer_fwd(cube, x, params, cfg, gs, c3.MODE_F32)
+        c3.transformer_layer_bwd(cube, dy, saved, params, cfg, c3.MODE_F32, grads=grads)
+
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = dist.max_over_ranks(e0.elapsed_time(e1) / steps)
+    return {"value": b / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "dtype": "f32", "path": "MODE_F32: fp32 storage, SIMT fp32 GEMMs, eager"}
+
+
 # -------------------------------------------------------------------- our arm
 def make_layer_inputs(cube, wl, dtype):
     import torch
@@ -458,7 +503,7 @@ def our_arm(args, wl):
             mm = {"error": str(ex)}
 
     # ---- roofline of the dominant kernel (tcgen05 GEMM), live per-launch timing
-    peak_tc, peak_hbm, peak_src = measured_peaks()
+    peak_tc, peak_hbm, peak_src = measured_peaks(clk)
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     traffic = None
     tp = ROOT / "profiles" / "gemm_traffic.json"
@@ -484,14 +529,23 @@ def our_arm(args, wl):
     layer_roofline = {**bound, "bound_ms": max(bound.values()),
                       "frac": max(bound.values()) / ms_max,
                       "elements_sent_per_rank": sent,
-                      "note": "max(flops / (sustained bf16 peak x GPUs), elements sent per rank "
+                      "note": "max(flops / (bf16 peak x GPUs), elements sent per rank "
                               "x 2 B / 770 GB/s) / measured ms; HBM-bound kernels not included"}
+
+    f32 = None
+    if not args.no_fp32:
+        try:
+            f32 = fp32_mode_figure(cube, wl)
+        except Exception as ex:  # report, never fake
+            f32 = {"error": str(ex)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             dt, meta = cpu_reference_sample(wl)
             cpu = {"value": 2 / dt, "unit": UNIT, **meta}
+            cpu["fwd_seq_per_s"] = 2 / meta["fwd_s"]
+            cpu["bwd_seq_per_s"] = 2 / meta["bwd_s"]
         except Exception as ex:  # report, never fake
             cpu = {"value": None, "unit": UNIT, "error": str(ex)}
 
@@ -512,7 +566,7 @@ def our_arm(args, wl):
             "roofline": {"bound": "tensor", "kernel": "tc_gemm (tcgen05 + TMA, bf16->fp32)",
                          "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
                          "frac": achieved / peak_tc if peak_tc else None, "traffic": traffic,
-                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "peak_source": peak_src,
                          "launches_per_step": gemm_n / prof_steps,
                          "kernel_ms_per_step": gemm_ms / prof_steps,
                          "share_of_step": (gemm_ms / prof_steps) / ms_max,
@@ -523,6 +577,7 @@ def our_arm(args, wl):
             "matmul": mm,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
             "layer_roofline": layer_roofline,
+            "fp32_mode": f32,
             "collectives": {"calls_per_step": comm_n / prof_steps,
                             "ms_per_step": comm_ms / prof_steps,
                             "payload_mb_per_step": comm_bytes / prof_steps / 1e6,
@@ -537,14 +592,22 @@ def our_arm(args, wl):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    # Captured graphs still reference the NCCL communicators, and tearing those down
-    # under live graphs can block; every rank is past its last collective after this
-    # barrier, so leave process teardown to the OS.
+    # Orderly teardown (exit hooks must run): captured graphs first, since they hold
+    # the peer-memory collectives' buffers, then the cube (NCCL communicators, IPC
+    # mappings) after a barrier, then the process group.
     torch.cuda.synchronize()
     dist.barrier()
+    graph = None
+    outs.clear()
+    params = x = dy = grads = None
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
+    dist.barrier()
+    cube.close()
+    dist.destroy()
     sys.stdout.flush()
-    sys.stderr.flush()
-    os._exit(0)
+    return 0
 
 
 def main():
@@ -557,6 +620,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-exact mode figure")
     ap.add_argument("--no-matmul", action="store_true", help="skip the 3-D matmul TFLOP/s line")
     ap.add_argument("--grid", default=None,
                     help="px x py x pz (e.g. 4x1x1); default: 1x1x1, 2x1x1, 1x2x2, 2x2x2")

@@ -153,3 +153,15 @@ def run_verify(p=2, b=2, s=8, n=2, h=16, seed=7, f32=False):
     rc = lib().ref_run_verify(p, C.c_int64(b), C.c_int64(s), C.c_int64(n), C.c_int64(h),
                               C.c_uint64(seed), int(f32), buf, C.c_int64(1 << 16))
     return rc == 0, buf.value.decode()
+
+
+def time_layer(p, b, s, n, h, params, x, dy):
+    """The reference's 3-D layer fwd and bwd in float on p^3 rank threads, timed
+    separately with an Endpoint barrier between them: (fwd_seconds, bwd_seconds)."""
+    ps = [np.ascontiguousarray(params[f], dtype=np.float64) for f in FIELDS]
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    dy = np.ascontiguousarray(dy, dtype=np.float64)
+    secs = (C.c_double * 2)()
+    _chk(lib().ref_time_layer(p, C.c_int64(b), C.c_int64(s), C.c_int64(n), C.c_int64(h),
+                              _pp(ps), _dp(x), _dp(dy), secs))
+    return secs[0], secs[1]

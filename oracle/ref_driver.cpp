@@ -253,6 +253,50 @@ int ref_run_layer(int p, int f32, int64_t b, int64_t s, int64_t n, int64_t h,
   });
 }
 
+// The reference's own 3-D layer fwd and bwd (transformer_layer_fwd/bwd,
+// cube3d/transformer.hpp:116-148) on run_spmd's rank threads, float, with an
+// Endpoint barrier between the two so the forward and backward are timed
+// separately (SURVEY.md §8(d) "time fwd and bwd separately with a barrier").
+// Same partitioning as verify_detail::run_layer (cube3d/verify.hpp:182-202);
+// outputs are discarded: this entry is the CPU baseline clock, run_layer above
+// is the checker. seconds[0] = fwd, seconds[1] = bwd (rank 0's wall clock).
+int ref_time_layer(int p, int64_t b, int64_t s, int64_t n, int64_t h,
+                   const double* const* params, const double* x, const double* dy,
+                   double* seconds) {
+  return guard([&] {
+    TransformerConfig cfg = make_cfg(p, b, s, n, h);
+    cfg.validate();
+    CubeTopology topo(cfg.p);
+    auto gp = params_of<float>(cfg, params);
+    auto ps = partition_layer_params(gp, cfg, topo, 0);
+    auto xs = activation_from_global(to_mat<float>(x, b * s, h), cfg.batch, cfg.seq, 0, topo);
+    auto dys = activation_from_global(to_mat<float>(dy, b * s, h), cfg.batch, cfg.seq, 0, topo);
+    Transport<float> tr(topo, Scheduler::threads);
+    double tf = 0, tb = 0;
+    run_spmd(tr, [&](Endpoint<float>& ep) {
+      const int r = ep.rank();
+      GroupState gs{0};
+      LayerSaved<float> saved;
+      ep.barrier();
+      auto t0 = std::chrono::steady_clock::now();
+      auto y = transformer_layer_fwd(ep, xs[r], ps[r], cfg, gs, &saved);
+      ep.barrier();
+      auto t1 = std::chrono::steady_clock::now();
+      auto g = transformer_layer_bwd(ep, dys[r], saved, ps[r], cfg);
+      ep.barrier();
+      auto t2 = std::chrono::steady_clock::now();
+      if (r == 0) {
+        tf = std::chrono::duration<double>(t1 - t0).count();
+        tb = std::chrono::duration<double>(t2 - t1).count();
+      }
+      (void)y;
+      (void)g;
+    });
+    seconds[0] = tf;
+    seconds[1] = tb;
+  });
+}
+
 // Serial reference layer (ref_layer_fwd/bwd, cube3d/reference.hpp:301-354), float64.
 int ref_layer_serial(int64_t b, int64_t s, int64_t n, int64_t h, const double* const* params,
                      const double* x, const double* dy, double* y, double* dx,

@@ -79,3 +79,9 @@ def barrier():
     import torch.distributed as dist
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.barrier()
+
+
+def destroy():
+    import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
