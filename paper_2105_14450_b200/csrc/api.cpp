@@ -284,7 +284,7 @@ int c3d_diagonal_slice(const int dims[3], const int coords[3], int64_t global_le
     auto c = coords3(coords);
     g.check(c);
     auto r = c3d::diagonal_slice(g, c, global_len);
-    if (holds) *holds = c3d::diagonal_holder(c) ? 1 : 0;
+    if (holds) *holds = c3d::diagonal_holder(g, c) ? 1 : 0;
     out[0] = r.begin;
     out[1] = r.end;
   });

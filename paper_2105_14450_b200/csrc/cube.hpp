@@ -109,6 +109,12 @@ class Cube {
   c3d_counters& counters() { return counters_; }
   const c3d_counters& counters() const { return counters_; }
   void add_madds(uint64_t n) { counters_.multiply_adds += n; }
+
+  // Persistent device workspace that is all-zero between uses (kernels that use it
+  // restore the zeros, e.g. the flash backward's fp32 dQ accumulator). Grows on demand
+  // outside stream capture; returns nullptr when it would have to grow while `s` is
+  // being captured (the caller then uses a stream-ordered buffer of its own).
+  void* zero_workspace(size_t bytes, cudaStream_t s);
   void reset_counters() { std::memset(&counters_, 0, sizeof(counters_)); }
 
  private:
@@ -125,6 +131,8 @@ class Cube {
   std::unique_ptr<SymmHeap> symm_;  // peer-memory transport (null: NCCL for everything)
   std::vector<int> line_[3];        // world ranks of this rank's axis lines, by position
   c3d_counters counters_{};
+  void* zero_ws_ = nullptr;
+  size_t zero_ws_bytes_ = 0;
 };
 
 }  // namespace c3d

@@ -18,7 +18,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
 bool tc_gemm_rs_supported(const GemmProblem& p, int bn);
 int tc_gemm_grid(const GemmProblem& p, int bn, int num_sms);
 
-// TMA maps for the other tcgen05 kernels (attention.cu): a 5-D operand map (box
+// TMA maps for the other tcgen05 kernels (flash.cu): a 5-D operand map (box
 // 64 K-columns x box_rows rows, 128B swizzle; MN-major views get 64 x 64 boxes) and a
 // store/load map with an explicit box (128B swizzle).
 CUtensorMap tc_operand_map(const View& v, long long rows, long long cols, int batch, int box_rows,

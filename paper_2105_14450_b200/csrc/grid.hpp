@@ -10,6 +10,7 @@
 // its divisibility errors (both dimensions divisible by p^2).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <string>
@@ -166,19 +167,32 @@ inline Bounds shard_bounds(int layout, const Grid& g, const std::array<int, 3>& 
   fail(C3D_ERR_INTERNAL, "unknown layout " + std::to_string(layout));
 }
 
-// Diagonal placement (cube3d/layout.hpp:134-142), requires py == pz:
-// rank (i, j, l) holds b[j*N/q + i*N/(q*px), +N/(q*px)) iff j == l, q = py = pz.
-inline bool diagonal_holder(const std::array<int, 3>& c) { return c[1] == c[2]; }
+// Diagonal placement (cube3d/layout.hpp:134-142), generalised to py != pz.
+// The reference (py == pz == q): rank (i, j, l) holds b[j*N/q + i*N/(q*px), +N/(q*px))
+// iff j == l. Sub-grids with one of py, pz equal to 1 (the north star's 2x2x1): every
+// rank holds b[u*N/Q + i*N/(Q*px), +N/(Q*px)) with Q = max(py, pz) and u its coordinate
+// on the longer of the two axes -- each (i, u) owns one slice, and expand_diagonal /
+// reduce_to_diagonal gather / reduce along that axis instead of broadcasting from the
+// diagonal. Other py != pz grids have no consistent rule (the slice index would depend on
+// the direction triple) and are rejected.
+inline void require_diagonal_grid(const Grid& g) {
+  const int py = g.dims[1], pz = g.dims[2];
+  if (py != pz && py != 1 && pz != 1)
+    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need py == pz or one of them 1, got " +
+                                     std::to_string(py) + " and " + std::to_string(pz));
+}
+inline bool diagonal_holder(const Grid& g, const std::array<int, 3>& c) {
+  require_diagonal_grid(g);
+  return g.dims[1] == g.dims[2] ? c[1] == c[2] : true;
+}
 inline Range diagonal_slice(const Grid& g, const std::array<int, 3>& c, int64_t len) {
-  if (g.dims[1] != g.dims[2])
-    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need py == pz, got " +
-                                     std::to_string(g.dims[1]) + " and " +
-                                     std::to_string(g.dims[2]));
-  const int64_t q = g.dims[1], r = g.dims[0];
-  if (g.cubic()) require_divisible(len, q * q, "vector length");
-  require_divisible(len, q * r, "vector length");
-  const int64_t n2 = len / (q * r);
-  const int64_t b0 = static_cast<int64_t>(c[1]) * (len / q) + static_cast<int64_t>(c[0]) * n2;
+  require_diagonal_grid(g);
+  const int64_t Q = std::max(g.dims[1], g.dims[2]), r = g.dims[0];
+  if (g.cubic()) require_divisible(len, Q * Q, "vector length");
+  require_divisible(len, Q * r, "vector length");
+  const int64_t n2 = len / (Q * r);
+  const int64_t u = g.dims[1] >= g.dims[2] ? c[1] : c[2];
+  const int64_t b0 = u * (len / Q) + static_cast<int64_t>(c[0]) * n2;
   return {b0, b0 + n2};
 }
 

@@ -5,6 +5,7 @@
 // config 3) becomes batched GEMMs over all local (batch, head) slices with one
 // collective per step, and residual adds / bias / GELU / GELU' are fused into
 // GEMM epilogues whenever no reduce-scatter intervenes.
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -59,18 +60,17 @@ void validate_config(const Cube& cube, const Config& cfg) {
   const Grid& g = cube.grid();
   if (cfg.batch <= 0 || cfg.seq <= 0 || cfg.heads <= 0 || cfg.hidden <= 0)
     fail(C3D_ERR_CONFIG_INVALID, "batch, seq, heads and hidden must be positive");
-  if (g.dims[1] != g.dims[2])
-    fail(C3D_ERR_CONFIG_INVALID, "layer ops need py == pz (got " + std::to_string(g.dims[1]) +
-                                     " and " + std::to_string(g.dims[2]) + ")");
-  const int64_t q = g.dims[1], r = g.dims[0];
+  require_diagonal_grid(g);  // py == pz (the reference's cube) or one of them 1
+  const int64_t py = g.dims[1], pz = g.dims[2], r = g.dims[0];
+  const int64_t Q = std::max(py, pz);
   if (cfg.batch % r) fail(C3D_ERR_CONFIG_INVALID, "batch must be divisible by px");
-  if (cfg.seq % q) fail(C3D_ERR_CONFIG_INVALID, "seq must be divisible by p");
-  const int64_t p2 = g.cubic() ? q * q : q * r;
+  if (cfg.seq % py || cfg.seq % pz) fail(C3D_ERR_CONFIG_INVALID, "seq must be divisible by p");
+  const int64_t p2 = g.cubic() ? Q * Q : Q * r;
   if (cfg.hidden % p2) fail(C3D_ERR_CONFIG_INVALID, "hidden must be divisible by p^2");
   if ((4 * cfg.hidden) % p2) fail(C3D_ERR_CONFIG_INVALID, "4*hidden must be divisible by p^2");
-  if (cfg.heads % q)
+  if (cfg.heads % py || cfg.heads % pz)
     fail(C3D_ERR_HEADS_INDIVISIBLE,
-         "heads=" + std::to_string(cfg.heads) + " not divisible by p=" + std::to_string(q));
+         "heads=" + std::to_string(cfg.heads) + " not divisible by p=" + std::to_string(Q));
   if (cfg.hidden % cfg.heads) fail(C3D_ERR_CONFIG_INVALID, "hidden must be divisible by heads");
 }
 
@@ -107,8 +107,9 @@ void linear_fwd(Cube& cube, int mode, const Act& x, const LinearP& p, int& group
   Mat c;
   c.data = y.data;
   c.dtype = y.dtype;
+  const ActRows ar{x.batch / cube.extent(kX), x.seq};
   ab_forward(cube, mode, xf, p.w, c, e, s, pre ? &pre->wg : nullptr,
-             saved ? &saved->a_full : nullptr);
+             saved ? &saved->a_full : nullptr, &ar);
   group = 1 - group;
   y = make_act(cube, y.data, y.dtype, x.batch, x.seq, p.w.gcols, group);
   if (saved) {
@@ -150,8 +151,9 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
     da.dtype = dx->dtype;
     dap = &da;
   }
+  const ActRows ar{dy.batch / cube.extent(kX), dy.seq};
   ab_backward(cube, mode, dyf, saved.x, p.w, dap, dw, dx_gelu_aux, s, wg, saved.a_full.ptr,
-              sinks ? &sinks->dw : nullptr);
+              sinks ? &sinks->dw : nullptr, &ar);
   if (dap) *dx = make_act(cube, dx->data, dx->dtype, dy.batch, dy.seq, saved.x.gcols, p.input_group);
 }
 
@@ -353,45 +355,56 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
   } else {
     qv = qkv_view(qkv.data, dt, a, 0, false);
   }
-  // scores = scale * Q K^T  ([slice][S][sl], fp32)
   const int64_t srows = static_cast<int64_t>(nslices) * a.S;
-  DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s));
-  S.probs = pb.get();
   const ActGeom cg = act_geom(cube.grid(), x.batch, x.seq, cfg.hidden, qkv.group);
   DevBuf& ctx_buf = S.keep(DevBuf(static_cast<size_t>(cg.bl * cg.sl * cg.hl) * dtype_size(dt), s));
   Act ctx = make_act(cube, ctx_buf.get(), dt, x.batch, x.seq, cfg.hidden, qkv.group);
-  // whole key range on this rank: scores, softmax and P V in one tcgen05 kernel
-  const bool fused = a.Ps == 1 && mode != C3D_MODE_F32 && dt == kBF16 &&
-                     attn_fwd_fused(qv, qkv_view(qkv.data, dt, a, 1, false),
-                                    qkv_view(qkv.data, dt, a, 2, true),
-                                    scores_view(pb.get(), dt, a, false),
-                                    packed_out(ctx.data, dt, a, false), a.S, a.sl, a.dh, a.H,
-                                    nslices, a.scale, s);
-  if (fused) cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
-  // key range split along the seq axis: the distributed softmax of the reference
-  // (row max -> all-reduce(max) -> exp-sum -> all-reduce(sum) -> normalise) with the
-  // scores recomputed in TMEM by three passes of the fused kernel
-  bool fused_dist = false;
-  if (!fused && a.Ps > 1 && mode != C3D_MODE_F32 && dt == kBF16) {
-    DevBuf mx(static_cast<size_t>(srows) * sizeof(float), s);
-    DevBuf sm(static_cast<size_t>(srows) * sizeof(float), s);
-    DevBuf partial(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+  // Flash path (flash.cu): scores and probabilities stay on chip; the backward recomputes
+  // them from the saved row log-sum-exp. With the key range split along the seq axis,
+  // each rank's partial context is normalised over its own keys and the ranks' partials
+  // are combined with the reference's two statistic all-reduces (max, then sum;
+  // cube3d/attention.hpp:106-126) before the context reduce-scatter.
+  bool flashed = false;
+  if (mode != C3D_MODE_F32 && dt == kBF16 && flash_supported(a.S, a.sl, a.dh)) {
     const View kv = qkv_view(qkv.data, dt, a, 1, false), vv = qkv_view(qkv.data, dt, a, 2, true);
-    const View pv = scores_view(pb.get(), dt, a, false), cv = packed_out(partial.get(), dt, a, true);
-    if (attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 1,
-                       mx.as<float>(), sm.as<float>())) {
-      cube.all_reduce(a.seq_axis, mx.get(), srows, kF32, true, s);
-      attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 2,
-                     mx.as<float>(), sm.as<float>());
-      cube.all_reduce(a.seq_axis, sm.get(), srows, kF32, false, s);
-      attn_fwd_fused(qv, kv, vv, pv, cv, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, 3,
-                     mx.as<float>(), sm.as<float>());
-      cube.reduce_scatter(a.seq_axis, partial.get(), ctx.data, rows * a.hd, dt, s);
+    DevBuf& lb = S.keep(DevBuf(static_cast<size_t>(srows) * sizeof(float), s));
+    if (a.Ps == 1) {
+      flashed = flash_fwd(qv, kv, vv, packed_out(ctx.data, dt, a, false), lb.as<float>(), a.S,
+                          a.sl, a.dh, a.H, nslices, a.scale, s);
+    } else {
+      DevBuf partial(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+      DevBuf lr(static_cast<size_t>(srows) * sizeof(float), s);
+      const View pv = packed_out(partial.get(), dt, a, true);
+      flashed = flash_fwd(qv, kv, vv, pv, lr.as<float>(), a.S, a.sl, a.dh, a.H, nslices, a.scale, s);
+      if (flashed) {
+        C3D_CUDA(cudaMemcpyAsync(lb.get(), lr.get(), static_cast<size_t>(srows) * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+        cube.all_reduce(a.seq_axis, lb.get(), srows, kF32, true, s);
+        DevBuf w(static_cast<size_t>(srows) * sizeof(float), s);
+        k_flash_lse_weights(lr.as<float>(), lb.as<float>(), w.as<float>(), srows, s);
+        cube.all_reduce(a.seq_axis, w.get(), srows, kF32, false, s);
+        k_flash_combine(pv, lr.as<float>(), lb.as<float>(), w.as<float>(), a.S, a.dh, a.H,
+                        nslices, s);
+        cube.reduce_scatter(a.seq_axis, partial.get(), ctx.data, rows * a.hd, dt, s);
+      }
+    }
+    if (flashed) {
+      S.lse = lb.as<float>();
       cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
-      fused_dist = true;
     }
   }
-  if (!fused && !fused_dist) {
+  if (flashed) {
+    LinearEpi oe;
+    oe.resid = resid;
+    linear_fwd(cube, mode, ctx, out_p, group, y, &S.out_lin, false, oe, s, out_pre);
+    return;
+  }
+  // scores = scale * Q K^T  ([slice][S][sl], fp32)
+  DevBuf& pb = S.keep(DevBuf(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s));
+  S.probs = pb.get();
+  // unfused path (fp32-exact mode, shapes outside the flash kernels): scores GEMM,
+  // distributed softmax, P V GEMM
+  {
     DevBuf sc(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
     Epilogue e;
     e.out = scores_view(sc.get(), kF32, a, false);
@@ -412,7 +425,7 @@ void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const 
     }
   }
   // context = P V, reduce-scattered back to this rank's seq block
-  if (!fused && !fused_dist) {
+  {
     Epilogue e;
     DevBuf partial;
     if (a.Ps == 1) {
@@ -451,67 +464,55 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
   Gathered dcf = gather(cube, a.seq_axis, dctx.data, rows * a.hd, dt, s);
   DevBuf dqkv_buf(static_cast<size_t>(rows * a.ld_qkv) * dtype_size(dt), s);
   const int64_t srows = static_cast<int64_t>(nslices) * a.S;
-  DevBuf dp(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s);  // dS, activation dtype
-  // whole key range on this rank (bf16): the softmax backward is fused into the dP
-  // GEMM epilogue, dS = P * (dP - D) * scale with D = rowsum(dctx * ctx) = sum_j P dP
-  const bool fused_ds = a.Ps == 1 && mode != C3D_MODE_F32 && dt == kBF16 &&
-                        !std::getenv("C3D_NO_FUSED_ATTN");
-  DevBuf dpf;
-  bool fused_dq = false;  // dS and dQ from the fused attention-backward kernel
-  DevBuf dq_partial;      // split seq axis: the fused kernel's partial dQ, reduce-scattered
-  if (a.Ps > 1 && mode != C3D_MODE_F32 && dt == kBF16 && !std::getenv("C3D_NO_FUSED_ATTN")) {
-    // D = rowsum(dctx * ctx) on this rank's query rows, all-gathered along the seq axis
-    DevBuf rdl(static_cast<size_t>(nslices * a.sl) * sizeof(float), s);
-    k_attn_rowdot(dctx.data, S.out_lin.x.data, dt, nslices, a.sl, a.H, a.dh, a.sl * a.hd,
-                  rdl.as<float>(), s);
+  if (S.lse) {
+    // flash backward: D = rowsum(dctx * ctx) (all-gathered along the seq axis when the
+    // query rows are split), then dQ, dK, dV from recomputed probabilities
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
-    cube.all_gather(a.seq_axis, rdl.get(), rd.get(), static_cast<size_t>(nslices * a.sl), kF32, s);
-    dq_partial = DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
-    fused_dq = attn_bwd_fused(packed_view(dcf.ptr, dt, a, false), qkv_view(qkv, dt, a, 2, false),
-                              qkv_view(qkv, dt, a, 1, true), scores_view(S.probs, dt, a, false),
-                              scores_view(dp.get(), dt, a, false),
-                              packed_out(dq_partial.get(), dt, a, true), rd.as<float>(), a.S,
-                              a.sl, a.dh, a.H, nslices, a.scale, s, a.sl);
-    if (fused_dq) {
-      cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+    int64_t rd_split = 0;
+    if (a.Ps == 1) {
+      k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
+                    rd.as<float>(), s);
+    } else {
+      DevBuf rdl(static_cast<size_t>(nslices * a.sl) * sizeof(float), s);
+      k_attn_rowdot(dctx.data, S.out_lin.x.data, dt, nslices, a.sl, a.H, a.dh, a.sl * a.hd,
+                    rdl.as<float>(), s);
+      cube.all_gather(a.seq_axis, rdl.get(), rd.get(), static_cast<size_t>(nslices * a.sl), kF32, s);
+      rd_split = a.sl;
+    }
+    DevBuf ws_buf(flash_bwd_workspace_bytes(a.S, a.dh, nslices), s);
+    void* ws = ws_buf.get();
+    DevBuf dq_partial;
+    View dqv = qkv_view(dqkv_buf.get(), dt, a, 0, false);
+    if (a.Ps > 1) {
+      dq_partial = DevBuf(static_cast<size_t>(a.Ps * rows * a.hd) * dtype_size(dt), s);
+      dqv = packed_out(dq_partial.get(), dt, a, true);
+    }
+    const View qv = a.Ps > 1 ? packed_view(S.q_full, dt, a, false) : qkv_view(qkv, dt, a, 0, false);
+    if (!flash_bwd(qv, qkv_view(qkv, dt, a, 1, false), qkv_view(qkv, dt, a, 2, false),
+                   packed_view(dcf.ptr, dt, a, false), S.lse, rd.as<float>(), rd_split, dqv,
+                   qkv_view(dqkv_buf.get(), dt, a, 1, false), qkv_view(dqkv_buf.get(), dt, a, 2, false),
+                   ws, a.S, a.sl, a.dh, a.H, nslices, a.scale, s))
+      fail(C3D_ERR_INTERNAL, "flash attention backward rejected the forward's layout");
+    cube.add_madds(4ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
+    if (a.Ps > 1) {
       DevBuf dq(static_cast<size_t>(rows * a.hd) * dtype_size(dt), s);
       cube.reduce_scatter(a.seq_axis, dq_partial.get(), dq.get(), rows * a.hd, dt, s);
       k_copy_heads(dq.get(), a.hd, a.dh, dqkv_buf.get(), a.ld_qkv, 3 * a.dh, rows, a.H, a.dh, dt, s);
     }
+    Act dqkv = make_act(cube, dqkv_buf.get(), dt, dy.batch, dy.seq, 3 * cfg.hidden, dctx.group);
+    linear_bwd(cube, mode, dqkv, S.qkv_lin, qkv_p, &dx, &g.w_qkv, &g.b_qkv, nullptr, s, qkv_wg,
+               qkv_sinks);
+    return;
   }
-  if (fused_ds) {
-    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
-    k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
-                  rd.as<float>(), s);
-    fused_dq = attn_bwd_fused(packed_view(dcf.ptr, dt, a, false), qkv_view(qkv, dt, a, 2, false),
-                              qkv_view(qkv, dt, a, 1, true), scores_view(S.probs, dt, a, false),
-                              scores_view(dp.get(), dt, a, false),
-                              qkv_view(dqkv_buf.get(), dt, a, 0, false), rd.as<float>(), a.S, a.sl,
-                              a.dh, a.H, nslices, a.scale, s);
-    if (fused_dq) cube.add_madds(2ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
-  }
-  if (fused_ds && !fused_dq) {
-    DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
-    k_attn_rowdot(dcf.ptr, S.out_lin.x.data, dt, nslices, a.S, a.H, a.dh, a.sl * a.hd,
-                  rd.as<float>(), s);
-    Epilogue e;
-    e.out = scores_view(dp.get(), dt, a, false);
-    e.alpha = a.scale;
-    e.act = kActSoftmaxBwd;
-    e.aux = S.probs;
-    e.aux_dtype = dt;
-    e.rowvec = rd.as<float>();
-    e.rv_div = a.sl;
-    gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
-               qkv_view(qkv, dt, a, 2, false), e, s);
-  } else if (!fused_ds && !fused_dq) {
-    // dP = dctx_full V^T (fp32)
-    dpf = DevBuf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
+  // unfused path: dP = dctx_full V^T (fp32)
+  DevBuf dpf(static_cast<size_t>(srows * a.sl) * sizeof(float), s);
+  {
     Epilogue e;
     e.out = scores_view(dpf.get(), kF32, a, false);
     gemm_views(cube, mode, a.S, a.sl, a.dh, nslices, packed_view(dcf.ptr, dt, a, false),
                qkv_view(qkv, dt, a, 2, false), e, s);
   }
+  DevBuf dp(static_cast<size_t>(srows * a.sl) * dtype_size(dt), s);  // dS, activation dtype
   // dV = P^T dctx_full
   {
     Epilogue e;
@@ -520,8 +521,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                packed_view(dcf.ptr, dt, a, true), e, s);
   }
   // dS = P * (dP - rowdot) * scale, rowdot summed along the seq axis
-  if (fused_ds || fused_dq) {
-  } else if (a.Ps == 1) {
+  if (a.Ps == 1) {
     k_softmax_bwd_fused(dpf.as<float>(), S.probs, dt, srows, a.sl, a.scale, dp.get(), dt, s);
   } else {
     DevBuf rd(static_cast<size_t>(srows) * sizeof(float), s);
@@ -531,7 +531,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
                      dp.get(), dt, s);
   }
   // dQ = dS K (reduce-scattered), dK = dS^T Q_full
-  if (!fused_dq) {
+  {
     Epilogue e;
     DevBuf partial;
     if (a.Ps == 1) {

@@ -75,7 +75,8 @@ struct AttnSaved : Saved {
   LinearSaved qkv_lin, out_lin;
   Act qkv;                 // (b/px)(s/p_s) x 3h/p_h, head-major [head][q|k|v][dim]
   void* q_full = nullptr;  // gathered queries [p_s][rows][H*dh] (p_s > 1)
-  void* probs = nullptr;   // [b_loc*H][s][s_loc]
+  void* probs = nullptr;   // [b_loc*H][s][s_loc] (unfused paths)
+  float* lse = nullptr;    // [b_loc*H][s] row log-sum-exp, log2 units (flash path)
 };
 struct MlpSaved : Saved {
   LinearSaved fc1_lin, fc2_lin;

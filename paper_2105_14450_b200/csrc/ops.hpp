@@ -18,25 +18,28 @@ void prof_enable(bool on);
 void prof_read(double* ms, double* flops, long long* launches);
 void prof_read_comm(double* ms, double* bytes, long long* calls);
 
-// Fused attention core (attention.cu) for slices holding the whole key range: scores
-// in TMEM, softmax, probabilities saved to `probs`, context = P V into `ctx`. Returns
-// false (nothing launched) when the shapes are outside its limits.
-// mode 0: whole softmax locally; modes 1-3: distributed softmax over a split key range
-// (1 local row max -> stat_max, 2 row sum with the all-reduced max -> stat_sum, 3 P and
-// the partial context with both all-reduced).
-bool attn_fwd_fused(const View& q, const View& k, const View& v, const View& probs, const View& ctx,
-                    int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
-                    cudaStream_t s, int mode = 0, float* stat_max = nullptr,
-                    float* stat_sum = nullptr);
-
-// Fused attention backward core (attention.cu) for the same case: dP in TMEM, dS =
-// P * (dP - rowdot) * scale written to `ds` and used in shared memory for dQ = dS K.
+// Flash attention core (flash.cu), bf16, head dim 64 or 128, queries and keys multiples
+// of 128. Forward: ctx = softmax(scale q k^T) v per slice (normalised over this rank's
+// keys) and lse[slice][S] = log2-domain log-sum-exp of (scale log2e) q k^T. Backward:
+// dq, dk, dv from q, k, v, dO, lse and rowdot D = rowsum(dO * O); `ws` is an fp32
+// scratch of flash_bwd_workspace_bytes() (no initialisation needed).
 // `rd_split` > 0: rowdot is laid out [S / rd_split][slices][rd_split] (all-gathered along
-// the seq axis); d_o and dq may be row-split (gathered dO, partial dQ).
-bool attn_bwd_fused(const View& d_o, const View& v, const View& k_mn, const View& probs,
-                    const View& ds, const View& dq, const float* rowdot, int64_t S, int64_t keys,
-                    int64_t dh, int64_t H, int nslices, float scale, cudaStream_t s,
-                    int64_t rd_split = 0);
+// the seq axis); q / dO and dq may be row-split (gathered, partial). Both return false (nothing launched) outside the
+// supported shapes / layouts.
+bool flash_supported(int64_t S, int64_t keys, int64_t dh);
+bool flash_fwd(const View& q, const View& k, const View& v_mn, const View& ctx, float* lse,
+               int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
+               cudaStream_t s);
+// Key range split along the seq axis: w = exp2(lse_r - M) (M the all-reduced max), then
+// partial *= exp2(lse_r - M) / W (W the all-reduced sum of w) and lse_io: M -> M + log2 W.
+void k_flash_lse_weights(const float* lr, const float* mx, float* w, int64_t n, cudaStream_t s);
+void k_flash_combine(const View& partial, const float* lr, float* lse_io, const float* W, int64_t S,
+                     int64_t dh, int64_t H, int nslices, cudaStream_t s);
+size_t flash_bwd_workspace_bytes(int64_t S, int64_t dh, int nslices);
+bool flash_bwd(const View& q, const View& k, const View& v, const View& d_o, const float* lse,
+               const float* rowdot, int64_t rd_split, const View& dq, const View& dk, const View& dv,
+               void* ws, int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
+               cudaStream_t s);
 
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
@@ -99,6 +102,13 @@ void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
                               const std::vector<Vec>& outs, cudaStream_t s);
 
 // An operand already gathered along its axis: [P][shard] blocks `s_hi` elements apart.
+// Batch / sequence structure of an activation operand (Activation3D rows are [batch][seq]);
+// needed by the linear on grids with py != pz, where the row blocks of a gather / scatter
+// along the input and output axes interleave differently.
+struct ActRows {
+  int64_t bl = 0;   // local batch (b / px)
+  int64_t seq = 0;  // global sequence length
+};
 struct Operand {
   const void* ptr = nullptr;
   long long s_hi = 0;
@@ -138,13 +148,14 @@ struct LinearEpi {
 // `bg`: B already gathered along x (skips the gather). `keep_a`: receives the gathered A
 // (the caller keeps it for the backward instead of re-gathering, cube3d/ops3d.hpp:160).
 void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& epi,
-                cudaStream_t s, const Operand* bg = nullptr, Gathered* keep_a = nullptr);
+                cudaStream_t s, const Operand* bg = nullptr, Gathered* keep_a = nullptr,
+                const ActRows* ar = nullptr);
 // dA = dC B^T (RS along d.in), dB = A^T dC (RS along x); either output may be skipped
 // (data == nullptr). `da_epi_aux`: if set, dA *= gelu'(aux) is fused (aux in dA layout).
 // `bg` / `ag`: pre-gathered B (along x) / A (along d.in). `dw`: write the dB partial into
 // a packed sink instead of reduce-scattering it here.
 void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
                  Mat* db, const void* da_gelu_aux, cudaStream_t s, const Operand* bg = nullptr,
-                 const void* ag = nullptr, const DwSink* dw = nullptr);
+                 const void* ag = nullptr, const DwSink* dw = nullptr, const ActRows* ar = nullptr);
 
 }  // namespace c3d

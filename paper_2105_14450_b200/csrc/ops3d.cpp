@@ -138,75 +138,78 @@ Gathered gather(Cube& cube, int axis, const void* shard, size_t count, int dtype
 
 // ---------------------------------------------------------------- vectors
 
+// Extents of the two alternating axes for the diagonal collectives: the cube rule
+// (Pi == Po) broadcasts from the diagonal rank; with Pi == 1 every rank already holds
+// its output block's slices; with Po == 1 the blocks of the whole input-axis line are
+// gathered (grid.hpp, generalised diagonal placement).
+namespace {
+struct DiagPlan {
+  int Pi, Po, px;
+  bool cube_rule() const { return Pi == Po; }
+  bool gather_in() const { return Pi > Po; }  // Po == 1
+};
+DiagPlan diag_plan(const Cube& cube, const Dirs& d) {
+  const Grid& g = cube.grid();
+  require_diagonal_grid(g);
+  DiagPlan p{g.dims[d.in], g.dims[d.out], g.dims[kX]};
+  if (p.Pi != p.Po && p.Pi != 1 && p.Po != 1)
+    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need equal input/output axis extents or one of "
+                                 "them 1");
+  return p;
+}
+}  // namespace
+
 DevBuf expand_diagonal(Cube& cube, const Dirs& d, const Vec& v, cudaStream_t s) {
   const Grid& g = cube.grid();
+  const DiagPlan pl = diag_plan(cube, d);
   const Range sl = diagonal_slice(g, cube.coords(), v.len);
   const int64_t n2 = sl.size();
-  const int px = g.dims[kX];
-  if (g.dims[d.in] != g.dims[d.out])
-    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need equal input/output axis extents");
-  DevBuf out(static_cast<size_t>(n2 * px) * sizeof(float), s);
+  const int px = pl.px;
+  const int64_t out_len = n2 * px * (pl.gather_in() ? pl.Pi : 1);
+  DevBuf out(static_cast<size_t>(out_len) * sizeof(float), s);
   if (g.size() == 1) {
     k_convert(v.data, v.dtype, out.get(), kF32, n2, s);
     return out;
   }
-  // broadcast the holder's slice along the operand's input axis from position
-  // owner[d.out] (the diagonal rank of that line), then all-gather along x.
+  // cube rule: broadcast the holder's slice along the operand's input axis from position
+  // owner[d.out] (the diagonal rank of that line); then all-gather along x, and along
+  // the input axis when the output axis is not partitioned.
   DevBuf piece(static_cast<size_t>(n2) * dtype_size(v.dtype), s);
-  if (diagonal_holder(cube.coords()))
+  if (diagonal_holder(g, cube.coords()))
     C3D_CUDA(cudaMemcpyAsync(piece.get(), v.data, n2 * dtype_size(v.dtype),
                              cudaMemcpyDeviceToDevice, s));
-  cube.broadcast(d.in, cube.coord(d.out), piece.get(), n2, v.dtype, s);
-  if (px == 1) {
-    k_convert(piece.get(), v.dtype, out.get(), kF32, n2, s);
-    return out;
+  if (pl.cube_rule() && pl.Pi > 1) cube.broadcast(d.in, cube.coord(d.out), piece.get(), n2, v.dtype, s);
+  DevBuf xfull;
+  const void* cur = piece.get();
+  if (px > 1) {
+    xfull = DevBuf(static_cast<size_t>(n2 * px) * dtype_size(v.dtype), s);
+    cube.all_gather(kX, piece.get(), xfull.get(), n2, v.dtype, s);
+    cur = xfull.get();
   }
-  DevBuf full(static_cast<size_t>(n2 * px) * dtype_size(v.dtype), s);
-  cube.all_gather(kX, piece.get(), full.get(), n2, v.dtype, s);
-  k_convert(full.get(), v.dtype, out.get(), kF32, n2 * px, s);
+  DevBuf infull;
+  if (pl.gather_in()) {
+    infull = DevBuf(static_cast<size_t>(out_len) * dtype_size(v.dtype), s);
+    cube.all_gather(d.in, cur, infull.get(), n2 * px, v.dtype, s);
+    cur = infull.get();
+  }
+  k_convert(cur, v.dtype, out.get(), kF32, out_len, s);
   return out;
 }
 
 void reduce_to_diagonal(Cube& cube, const Dirs& d, const float* colsums, int nvec,
                         const Vec* outs, cudaStream_t s) {
-  const Grid& g = cube.grid();
-  const int64_t len = outs[0].len;
-  const Range sl = diagonal_slice(g, cube.coords(), len);
-  const int64_t n2 = sl.size();
-  const int px = g.dims[kX];
-  const int64_t block = n2 * px;  // per-vector column-sum length (len / p_out)
-  const bool holder = diagonal_holder(cube.coords());
-  for (int k = 0; k < nvec; ++k)
-    if (holder && outs[k].data == nullptr)
-      fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
-  if (g.size() == 1) {
-    for (int k = 0; k < nvec; ++k) k_convert(colsums + k * block, kF32, outs[k].data, outs[k].dtype, n2, s);
-    return;
-  }
-  // reduce-scatter along x: each vector's block splits into px slices; pack the
-  // slices position-major so one collective serves all vectors.
-  DevBuf packed(static_cast<size_t>(nvec * block) * sizeof(float), s);
-  for (int q = 0; q < px; ++q)
-    for (int k = 0; k < nvec; ++k)
-      C3D_CUDA(cudaMemcpyAsync(packed.as<float>() + (q * nvec + k) * n2,
-                               colsums + k * block + q * n2, n2 * sizeof(float),
-                               cudaMemcpyDeviceToDevice, s));
-  DevBuf slice(static_cast<size_t>(nvec * n2) * sizeof(float), s);
-  cube.reduce_scatter(kX, packed.get(), slice.get(), nvec * n2, kF32, s);
-  // sum along the operand's input axis (adjoint of the forward broadcast)
-  cube.all_reduce(d.in, slice.get(), nvec * n2, kF32, false, s);
-  if (holder)
-    for (int k = 0; k < nvec; ++k)
-      k_convert(slice.as<float>() + k * n2, kF32, outs[k].data, outs[k].dtype, n2, s);
+  std::vector<Vec> vs(outs, outs + nvec);
+  // one vector at a time is the packed form with one entry per vector
+  reduce_to_diagonal_multi(cube, d, colsums, vs, s);
 }
 
 DevBuf expand_diagonal_multi(Cube& cube, const Dirs& d, const std::vector<Vec>& vs,
                              std::vector<const float*>* blocks, cudaStream_t s) {
   const Grid& g = cube.grid();
-  const int px = g.dims[kX];
-  if (g.dims[d.in] != g.dims[d.out])
-    fail(C3D_ERR_CONFIG_INVALID, "diagonal vectors need equal input/output axis extents");
-  const bool holder = diagonal_holder(cube.coords());
+  const DiagPlan pl = diag_plan(cube, d);
+  const int px = pl.px;
+  const int G = pl.gather_in() ? pl.Pi : 1;  // input-axis blocks per expanded vector
+  const bool holder = diagonal_holder(g, cube.coords());
   std::vector<int64_t> n2(vs.size()), off(vs.size());
   int64_t S = 0;
   for (size_t k = 0; k < vs.size(); ++k) {
@@ -217,37 +220,46 @@ DevBuf expand_diagonal_multi(Cube& cube, const Dirs& d, const std::vector<Vec>& 
     if (holder && vs[k].data == nullptr)
       fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
   }
-  DevBuf out(static_cast<size_t>(S * px) * sizeof(float), s);
+  DevBuf out(static_cast<size_t>(S * px * G) * sizeof(float), s);
   blocks->assign(vs.size(), nullptr);
-  for (size_t k = 0; k < vs.size(); ++k) (*blocks)[k] = out.as<float>() + off[k] * px;
+  for (size_t k = 0; k < vs.size(); ++k) (*blocks)[k] = out.as<float>() + off[k] * px * G;
   if (g.size() == 1) {
     for (size_t k = 0; k < vs.size(); ++k)
       C3D_CUDA(cudaMemcpyAsync(out.as<float>() + off[k], vs[k].data, n2[k] * sizeof(float),
                                cudaMemcpyDeviceToDevice, s));
     return out;
   }
-  // holders pack their slices back to back, one broadcast along d.in, one gather along x
+  // holders pack their slices back to back: [k slice]; broadcast along d.in (cube rule),
+  // gather along x -> [q][k slice], along d.in (Po == 1) -> [u][q][k slice]
   DevBuf piece(static_cast<size_t>(S) * sizeof(float), s);
   if (holder)
     for (size_t k = 0; k < vs.size(); ++k)
       C3D_CUDA(cudaMemcpyAsync(piece.as<float>() + off[k], vs[k].data, n2[k] * sizeof(float),
                                cudaMemcpyDeviceToDevice, s));
-  cube.broadcast(d.in, cube.coord(d.out), piece.get(), S, kF32, s);
-  DevBuf full(static_cast<size_t>(S * px) * sizeof(float), s);
-  cube.all_gather(kX, piece.get(), full.get(), S, kF32, s);
-  // [q][k slice] -> per-vector column blocks [k][q slice]
+  if (pl.cube_rule() && pl.Pi > 1) cube.broadcast(d.in, cube.coord(d.out), piece.get(), S, kF32, s);
+  DevBuf full(static_cast<size_t>(S * px * G) * sizeof(float), s);
+  if (G > 1) {
+    DevBuf xf(static_cast<size_t>(S * px) * sizeof(float), s);
+    cube.all_gather(kX, piece.get(), xf.get(), S, kF32, s);
+    cube.all_gather(d.in, xf.get(), full.get(), S * px, kF32, s);
+  } else {
+    cube.all_gather(kX, piece.get(), full.get(), S, kF32, s);
+  }
+  // [u][q][k slice] -> per-vector blocks [k][u][q slice]
   for (size_t k = 0; k < vs.size(); ++k)
-    C3D_CUDA(cudaMemcpy2DAsync(out.as<float>() + off[k] * px, n2[k] * sizeof(float),
+    C3D_CUDA(cudaMemcpy2DAsync(out.as<float>() + off[k] * px * G, n2[k] * sizeof(float),
                                full.as<float>() + off[k], S * sizeof(float),
-                               n2[k] * sizeof(float), px, cudaMemcpyDeviceToDevice, s));
+                               n2[k] * sizeof(float), px * G, cudaMemcpyDeviceToDevice, s));
   return out;
 }
 
 void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
                               const std::vector<Vec>& outs, cudaStream_t s) {
   const Grid& g = cube.grid();
-  const int px = g.dims[kX];
-  const bool holder = diagonal_holder(cube.coords());
+  const DiagPlan pl = diag_plan(cube, d);
+  const int px = pl.px;
+  const int G = pl.gather_in() ? pl.Pi : 1;
+  const bool holder = diagonal_holder(g, cube.coords());
   std::vector<int64_t> n2(outs.size()), off(outs.size());
   int64_t S = 0;
   for (size_t k = 0; k < outs.size(); ++k) {
@@ -262,15 +274,28 @@ void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
       k_convert(colsums + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
     return;
   }
-  // column-sum blocks [k][q slice] -> position-major [q][k slice] for the reduce-scatter
-  DevBuf packed(static_cast<size_t>(S * px) * sizeof(float), s);
+  // column-sum blocks [k][u][q slice] -> position-major [u][q][k slice]; reduce-scatter
+  // along d.in (Po == 1), then along x; all-reduce along d.in (cube rule, the adjoint
+  // of the forward broadcast)
+  DevBuf packed(static_cast<size_t>(S * px * G) * sizeof(float), s);
   for (size_t k = 0; k < outs.size(); ++k)
     C3D_CUDA(cudaMemcpy2DAsync(packed.as<float>() + off[k], S * sizeof(float),
-                               colsums + off[k] * px, n2[k] * sizeof(float),
-                               n2[k] * sizeof(float), px, cudaMemcpyDeviceToDevice, s));
+                               colsums + off[k] * px * G, n2[k] * sizeof(float),
+                               n2[k] * sizeof(float), px * G, cudaMemcpyDeviceToDevice, s));
+  DevBuf xpart;
+  const float* cur = packed.as<float>();
+  if (G > 1) {
+    xpart = DevBuf(static_cast<size_t>(S * px) * sizeof(float), s);
+    cube.reduce_scatter(d.in, cur, xpart.get(), S * px, kF32, s);
+    cur = xpart.as<float>();
+  }
   DevBuf slice(static_cast<size_t>(S) * sizeof(float), s);
-  cube.reduce_scatter(kX, packed.get(), slice.get(), S, kF32, s);
-  cube.all_reduce(d.in, slice.get(), S, kF32, false, s);
+  if (px > 1) {
+    cube.reduce_scatter(kX, cur, slice.get(), S, kF32, s);
+  } else {
+    C3D_CUDA(cudaMemcpyAsync(slice.get(), cur, S * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  }
+  if (pl.cube_rule() && pl.Pi > 1) cube.all_reduce(d.in, slice.get(), S, kF32, false, s);
   if (holder)
     for (size_t k = 0; k < outs.size(); ++k)
       k_convert(slice.as<float>() + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
@@ -325,8 +350,25 @@ void mul_vec_bwd(Cube& cube, const Mat& dc, const Mat& a, const Vec& b, Mat& da,
 
 // ---------------------------------------------------------------- C = A B
 
+namespace {
+
+// dst[y][x][seg rows] = src[x][y][seg rows] (x < outer, y < inner): the row-block swap
+// between the [input-axis block][batch][seq] order of an all-gathered activation and the
+// [batch][seq] order of Activation3D (cube3d/activation.hpp:103-138) on grids with
+// py != pz. One strided copy per x.
+void swap_row_blocks(const void* src, void* dst, int64_t outer, int64_t inner, int64_t seg_rows,
+                     int64_t cols, int dtype, cudaStream_t s) {
+  const size_t blk = static_cast<size_t>(seg_rows * cols) * dtype_size(dtype);
+  for (int64_t x = 0; x < outer; ++x)
+    C3D_CUDA(cudaMemcpy2DAsync(static_cast<char*>(dst) + x * blk, outer * blk,
+                               static_cast<const char*>(src) + x * inner * blk, blk, blk, inner,
+                               cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace
+
 void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const LinearEpi& le,
-                cudaStream_t s, const Operand* bg, Gathered* keep_a) {
+                cudaStream_t s, const Operand* bg, Gathered* keep_a, const ActRows* ar) {
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // a: (M/(Pw Pin)) x (N/Pout); b: (N/Pout) x (K/(Pin Pw))
@@ -346,6 +388,19 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
   }
   c = make_mat(cube, c.data, c.dtype, a.grows, b.gcols, kOutput, d.swapped());
   Gathered af = gather(cube, d.in, a.data, a.elems(), a.dtype, s);  // (M/Pw) x (N/Pout)
+  if (ar && ar->bl > 1 && Pin != Pout) {
+    // activation rows (py != pz): the output's row blocks must follow the [batch][seq]
+    // order of the other group -- gathered [a][b][s] -> [b][a][s] (Pout == 1), or local
+    // [b][o][s] -> [o][b][s] before the reduce-scatter into Pout blocks (Pin == 1)
+    Gathered pa;
+    pa.buf = DevBuf(static_cast<size_t>(Mg * a.cols) * dtype_size(a.dtype), s);
+    if (Pin > Pout)
+      swap_row_blocks(af.ptr, pa.buf.get(), Pin, ar->bl, ar->seq / Pin, a.cols, a.dtype, s);
+    else
+      swap_row_blocks(af.ptr, pa.buf.get(), ar->bl, Pout, ar->seq / Pout, a.cols, a.dtype, s);
+    pa.ptr = pa.buf.get();
+    af = std::move(pa);
+  }
   View av = kmajor(af.ptr, a.dtype, a.cols);
   if (keep_a) *keep_a = std::move(af);  // buffer (if any) outlives this call
   Epilogue e;
@@ -378,7 +433,7 @@ void ab_forward(Cube& cube, int mode, const Mat& a, const Mat& b, Mat& c, const 
 
 void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b, Mat* da,
                  Mat* db, const void* da_gelu_aux, cudaStream_t s, const Operand* bg,
-                 const void* ag, const DwSink* dw) {
+                 const void* ag, const DwSink* dw, const ActRows* ar) {
   const Dirs d = a.dirs;
   const int Pin = cube.extent(d.in), Pw = cube.extent(d.w), Pout = cube.extent(d.out);
   // dC: (M/(Pw Pout)) x (K/Pin) with triple d.swapped(): gather along d.out
@@ -407,9 +462,33 @@ void ab_backward(Cube& cube, int mode, const Mat& dc, const Mat& a, const Mat& b
       bv.s_hi = b_hi;
     }
     need_dcf();
-    View av = kmajor(dcf.ptr, dc.dtype, Kc);
+    // activation rows (py != pz), the adjoint of ab_forward's swaps: dC [b][a][s] ->
+    // [a][b][s] before the reduce-scatter along d.in (Pout == 1); dA [o][b][s] -> [b][o][s]
+    // after the product (Pin == 1)
+    const bool swap = ar && ar->bl > 1 && Pin != Pout;
+    DevBuf dcp;
+    const void* dca = dcf.ptr;
+    if (swap && Pin > Pout) {
+      dcp = DevBuf(static_cast<size_t>(Mrows * Kc) * dtype_size(dc.dtype), s);
+      swap_row_blocks(dcf.ptr, dcp.get(), ar->bl, Pin, ar->seq / Pin, Kc, dc.dtype, s);
+      dca = dcp.get();
+    }
+    View av = kmajor(dca, dc.dtype, Kc);
     Epilogue e;
-    if (Pin == 1) {
+    if (swap && Pin < Pout) {
+      DevBuf tmp(static_cast<size_t>(Mrows * b.rows) * dtype_size(da->dtype), s);
+      e.out = out_view(tmp.get(), da->dtype, b.rows);
+      local_gemm(cube, mode, Mrows, b.rows, Kc, av, bv, e, s);
+      swap_row_blocks(tmp.get(), da->data, Pout, ar->bl, ar->seq / Pout, b.rows, da->dtype, s);
+      if (da_gelu_aux) {
+        Epilogue f;
+        f.out = out_view(da->data, da->dtype, da->cols);
+        f.act = kActMulAux;
+        f.aux = da_gelu_aux;
+        f.aux_dtype = da->dtype;
+        k_apply_epilogue(da->data, da->dtype, da->rows, da->cols, f, s);
+      }
+    } else if (Pin == 1) {
       e.out = out_view(da->data, da->dtype, da->cols);
       if (da_gelu_aux) {
         e.act = kActMulAux;

@@ -113,8 +113,9 @@ def build_cube(total_ranks: int) -> int:
 
 
 def grid_for(n_gpus: int) -> Tuple[int, int, int]:
-    """Grid used for n GPUs: 1 -> 1x1x1, 2 -> 2x1x1, 4 -> 1x2x2, 8 -> 2x2x2 (cube)."""
-    table = {1: (1, 1, 1), 2: (2, 1, 1), 4: (1, 2, 2), 8: (2, 2, 2)}
+    """Grid used for n GPUs (north star): 1 -> 1x1x1, 2 -> 2x1x1, 4 -> 2x2x1 sub-cubes,
+    8 -> the 2x2x2 cube."""
+    table = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
     if n_gpus in table:
         return table[n_gpus]
     p = build_cube(n_gpus)

@@ -149,15 +149,26 @@ def test_activation_roundtrip_subgrids(dims):
 
 
 def test_diagonal_subgrids_tile_once():
-    for dims in [(2, 1, 1), (1, 2, 2), (2, 2, 2), (3, 2, 2)]:
-        n = 24
+    # the reference's diagonal on cubes and py == pz grids; every rank holds one slice on
+    # sub-grids with py or pz equal to 1 (2x2x1, the north star's 4-GPU grid)
+    for dims in [(2, 1, 1), (1, 2, 2), (2, 2, 2), (3, 2, 2), (2, 2, 1), (2, 1, 2), (1, 4, 1)]:
+        n = 48
         fam = c3.partition_diagonal(np.arange(n, dtype=np.float64), dims)
         assert c3.collect_diagonal(fam, dims, n).tolist() == list(range(n))
+        holders = [c for c in c3._ranks(dims) if c3.diagonal_slice(dims, c, n)[0]]
+        if dims[1] == dims[2]:
+            assert all(c[1] == c[2] for c in holders)
+        else:
+            assert len(holders) == dims[0] * dims[1] * dims[2]
+    # 2x2x1: rank (i, j, 0) holds b[j*N/2 + i*N/4, +N/4)
+    assert c3.diagonal_slice((2, 2, 1), (1, 0, 0), 8) == (True, (2, 4))
+    assert c3.diagonal_slice((2, 2, 1), (0, 1, 0), 8) == (True, (4, 6))
     with pytest.raises(C3DError) as e:
-        c3.diagonal_slice((2, 2, 1), (0, 0, 0), 8)
+        c3.diagonal_slice((1, 2, 4), (0, 0, 0), 16)
     assert e.value.name == "ConfigInvalid"
 
 
 def test_grid_for_gpu_counts():
+    """BASELINE.json north star: 2 and 4 GPUs as the 2x1x1 and 2x2x1 sub-cubes."""
     assert c3.grid_for(1) == (1, 1, 1) and c3.grid_for(8) == (2, 2, 2)
-    assert c3.grid_for(2) == (2, 1, 1) and c3.grid_for(4) == (1, 2, 2)
+    assert c3.grid_for(2) == (2, 1, 1) and c3.grid_for(4) == (2, 2, 1)

@@ -76,8 +76,8 @@ def compare_bf16(y, dx, gr, gp, x, dy, b, s, n):
 
 @pytest.mark.parametrize("shape", [(4, 128, 4, 256), (2, 256, 4, 256), (2, 512, 16, 1024)])
 def test_layer_bf16_tensor_core_shapes(cube, shape):
-    """Shapes where every GEMM takes the tcgen05 path (dh = 64), vs the oracle; s = 256 and
-    512 also take the fused attention kernel (scores in TMEM)."""
+    """Shapes where every GEMM takes the tcgen05 path and the attention the flash kernels
+    (dh = 64), vs the oracle."""
     b, s, n, h = shape
     r = O.Rng(99)
     P = O.init_layer_params(h, 99)
@@ -90,22 +90,24 @@ def test_layer_bf16_tensor_core_shapes(cube, shape):
     compare_bf16(y, dx, gr, gp, x, dy, b, s, n)
 
 
-def test_fused_attention_matches_unfused(cube, monkeypatch):
-    """The fused attention kernel (scores/softmax/PV in one tcgen05 kernel) against the
-    unfused path (scores GEMM -> softmax kernel -> P V GEMM) on the same inputs."""
+def test_flash_attention_layer_matches_unfused(cube, monkeypatch):
+    """The layer with the flash attention kernels (scores and probabilities never in HBM)
+    against the unfused path (scores GEMM -> softmax kernel -> P V GEMM and the GEMM
+    backward) on the same bf16 inputs. The two round P at different points (normalised
+    vs unnormalised before bf16), hence the bf16-level tolerance."""
     b, s, n, h = 2, 512, 8, 512
     r = O.Rng(17)
     P = O.init_layer_params(h, 17)
     gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
     x = bf16_round(O.random_matrix(b * s, h, r))
     dy = bf16_round(O.random_matrix(b * s, h, r))
-    fused = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
-    monkeypatch.setenv("C3D_NO_FUSED_ATTN", "1")
+    flash = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
+    monkeypatch.setenv("C3D_NO_FLASH", "1")
     plain = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
-    assert O.normwise_err(fused[0], plain[0]) < 2e-3
-    assert O.normwise_err(fused[1], plain[1]) < 5e-3
+    assert O.normwise_err(flash[0], plain[0]) < 1e-2
+    assert O.normwise_err(flash[1], plain[1]) < 1e-2
     for f in O.FIELDS:
-        assert O.normwise_err(fused[2][f], plain[2][f]) < 5e-3, f
+        assert O.normwise_err(flash[2][f], plain[2][f]) < 1e-2, f
 
 
 def test_layer_fp32_mid_shape(cube):
@@ -184,21 +186,3 @@ def test_transformer_stack_two_layers(cube, dtype, mode):
         for f in O.FIELDS:
             got = to_np(getattr(grads[k], f).shard)
             assert O.normwise_err(got, getattr(G, f).reshape(got.shape)) < tol, (k, f)
-
-
-def test_fused_attention_backward_matches_gemm_path(cube, monkeypatch):
-    """The fused attention-backward kernel (dP in TMEM, dS in place, dQ = dS K) against the
-    GEMM path with the softmax backward in the dP epilogue, same inputs."""
-    b, s, n, h = 2, 512, 8, 512
-    r = O.Rng(23)
-    P = O.init_layer_params(h, 23)
-    gp = c3.GlobalLayerParams(**{f: bf16_round(getattr(P, f)) for f in O.FIELDS})
-    x = bf16_round(O.random_matrix(b * s, h, r))
-    dy = bf16_round(O.random_matrix(b * s, h, r))
-    fused = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
-    monkeypatch.setenv("C3D_NO_FUSED_ATTN_BWD", "1")
-    plain = run_layer(cube, gp, x, dy, b, s, n, h, c3.BF16, c3.MODE_AUTO)
-    assert np.array_equal(fused[0], plain[0])
-    assert O.normwise_err(fused[1], plain[1]) < 5e-3
-    for f in O.FIELDS:
-        assert O.normwise_err(fused[2][f], plain[2][f]) < 5e-3, f

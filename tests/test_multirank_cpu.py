@@ -29,7 +29,7 @@ def _worker(rank, world, port, out_q):
         uid = cdist.exchange_uid(rank, world, uid_fn=lambda: bytes(range(128)))
         dims = c3.grid_for(world)
         coords = c3.coords_of(dims, rank)
-        b, s, h = 4, 8, 16
+        b, s, h = 4, 8, 16  # divisible on 2x1x1, 2x2x1 and 2x2x2
         g = np.arange(b * s * h, dtype=np.float64).reshape(b * s, h)
         w = np.arange(16 * 32, dtype=np.float64).reshape(16, 32)
         v = np.arange(48, dtype=np.float64)
@@ -51,7 +51,7 @@ def _worker(rank, world, port, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_gloo_multirank_placement(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_blocks_gpu.py -x -q 2>&1 | tail -3
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:flash -s 2 -c 2 --csv python tools/profile_step.py 3 2>/dev/null | grep flash | awk -F'","' '{print $5, $NF}'
+C3D_FLASH_TRACE=1 python tools/profile_step.py 1 2>&1 | grep "it  [0-9]:\|it 1[0-5]:" | tail -16

@@ -246,7 +246,7 @@ def main():
     collective_checks(cube, dims)
     if os.environ.get("MP_SKIP_MATMUL") is None:
         matmul_checks(cube, dims)
-    if dims[1] == dims[2]:
+    if dims[1] == dims[2] or 1 in dims[1:]:  # layer grids: py == pz or one of them 1
         loss_check(cube, dims)
         layer_tc_check(cube, dims)
         for name in ("layer_toy", "layer_small"):
