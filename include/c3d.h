@@ -21,7 +21,8 @@
  * enqueued (cube3d/ops3d.hpp:117-124).
  *
  * Grids generalise the reference's p x p x p cube (cube3d/topology.hpp:57-118)
- * to px x py x pz; layer ops additionally require py == pz.
+ * to px x py x pz; layer ops (and diagonal vectors) need py == pz -- the reference's
+ * rule -- or one of py, pz equal to 1, e.g. the 2x2x1 sub-cube.
  */
 #ifndef C3D_H_
 #define C3D_H_
@@ -124,7 +125,8 @@ int c3d_build_cube(int total_ranks, int* side);
  * out = {row_begin, row_end, col_begin, col_end}. dirs = {input, weight, output}. */
 int c3d_shard_bounds(int layout, const int dims[3], const int coords[3], int64_t rows,
                      int64_t cols, const int dirs[3], int64_t out[4]);
-/* diagonal_holder / diagonal_slice (cube3d/layout.hpp:134-142). out = {begin, end}. */
+/* diagonal_holder / diagonal_slice (cube3d/layout.hpp:134-142). out = {begin, end}.
+ * On py != pz grids with min(py, pz) = 1 every rank holds a slice. */
 int c3d_diagonal_slice(const int dims[3], const int coords[3], int64_t global_len,
                        int* holds, int64_t out[2]);
 /* activation_from_global's index map (cube3d/activation.hpp:103-138): global row of
@@ -162,6 +164,14 @@ int c3d_cube_info(const c3d_cube* cube, int* rank, int coords[3], int dims[3]);
 /* Endpoint::barrier (cube3d/transport.hpp:260-266), stream-ordered. */
 int c3d_cube_barrier(c3d_cube* cube, void* stream);
 int c3d_counters_get(const c3d_cube* cube, c3d_counters* out);
+/* Synchronises `stream` and reports whether any peer-memory wait of this cube failed:
+ * a peer that did not arrive within C3D_PEER_TIMEOUT_MS (default 30 s) or a collective
+ * whose (kind, root, op, dtype, count) header differs between the members of a line
+ * (the reference's RoundHeader check, cube3d/transport.hpp:32-40, 305-319). Then returns
+ * C3D_ERR_DESYNC and the cube stays poisoned: every later operation on it fails with
+ * C3D_ERR_DESYNC too (the reference poisons the group, transport.hpp:67-78). Operations
+ * check the record at entry, so a failure is also reported by the next call. */
+int c3d_cube_check(c3d_cube* cube, void* stream);
 int c3d_counters_reset(c3d_cube* cube);
 
 /* Endpoint collectives along one axis line (cube3d/transport.hpp:160-257), device

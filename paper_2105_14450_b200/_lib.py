@@ -105,6 +105,7 @@ SIGNATURES = {
     "c3d_cube_barrier": [VP, VP],
     "c3d_counters_get": [VP, P(c3d_counters)],
     "c3d_counters_reset": [VP],
+    "c3d_cube_check": [VP, VP],
     "c3d_broadcast": [VP, C.c_int, C.c_int, VP, C.c_size_t, C.c_int, VP],
     "c3d_all_gather": [VP, C.c_int, VP, VP, C.c_size_t, C.c_int, VP],
     "c3d_reduce_scatter": [VP, C.c_int, VP, VP, C.c_size_t, C.c_int, VP],

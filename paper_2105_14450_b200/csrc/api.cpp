@@ -56,9 +56,17 @@ int guard(F&& f) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-c3d::Cube& get(c3d_cube* c) {
+// Every operation entry checks the cube's fault record first (cheap host read): a peer
+// wait that failed in an earlier kernel makes this and every later call fail with
+// C3D_ERR_DESYNC.
+c3d::Cube& peek(c3d_cube* c) {
   if (!c || !c->impl) c3d::fail(C3D_ERR_CONFIG_INVALID, "null cube handle");
   return *c->impl;
+}
+c3d::Cube& get(c3d_cube* c) {
+  c3d::Cube& cube = peek(c);
+  cube.check_fault();
+  return cube;
 }
 
 void need(const void* p, const char* what) {
@@ -334,7 +342,7 @@ int c3d_cube_destroy(c3d_cube* cube) {
 }
 int c3d_cube_info(const c3d_cube* cube, int* rank, int coords[3], int dims[3]) {
   return guard([&] {
-    auto& c = get(const_cast<c3d_cube*>(cube));
+    auto& c = peek(const_cast<c3d_cube*>(cube));
     if (rank) *rank = c.rank();
     for (int a = 0; a < 3; ++a) {
       if (coords) coords[a] = c.coords()[a];
@@ -346,7 +354,14 @@ int c3d_cube_barrier(c3d_cube* cube, void* stream) {
   return guard([&] { get(cube).barrier(as_stream(stream)); });
 }
 int c3d_counters_get(const c3d_cube* cube, c3d_counters* out) {
-  return guard([&] { *out = get(const_cast<c3d_cube*>(cube)).counters(); });
+  return guard([&] { *out = peek(const_cast<c3d_cube*>(cube)).counters(); });
+}
+int c3d_cube_check(c3d_cube* cube, void* stream) {
+  return guard([&] {
+    auto& c = peek(cube);
+    C3D_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    c.check_fault();
+  });
 }
 int c3d_counters_reset(c3d_cube* cube) {
   return guard([&] { get(cube).reset_counters(); });

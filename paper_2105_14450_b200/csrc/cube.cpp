@@ -75,6 +75,11 @@ Cube::~Cube() {
   if (world_) ncclCommDestroy(world_);
 }
 
+void Cube::check_fault() {
+  if (poisoned_.empty() && symm_) poisoned_ = symm_->fault_message();
+  if (!poisoned_.empty()) fail(C3D_ERR_DESYNC, "rank " + std::to_string(rank_) + ": " + poisoned_);
+}
+
 void* Cube::zero_workspace(size_t bytes, cudaStream_t s) {
   if (bytes <= zero_ws_bytes_) return zero_ws_;
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;

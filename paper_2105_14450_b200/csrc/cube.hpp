@@ -110,6 +110,11 @@ class Cube {
   const c3d_counters& counters() const { return counters_; }
   void add_madds(uint64_t n) { counters_.multiply_adds += n; }
 
+  // Fails with C3D_ERR_DESYNC when a peer-memory wait of an earlier (completed) kernel
+  // timed out or saw a mismatched collective header; the cube then stays poisoned, as
+  // the reference poisons a group whose collective failed (cube3d/transport.hpp:67-78).
+  void check_fault();
+
   // Persistent device workspace that is all-zero between uses (kernels that use it
   // restore the zeros, e.g. the flash backward's fp32 dQ accumulator). Grows on demand
   // outside stream capture; returns nullptr when it would have to grow while `s` is
@@ -131,6 +136,7 @@ class Cube {
   std::unique_ptr<SymmHeap> symm_;  // peer-memory transport (null: NCCL for everything)
   std::vector<int> line_[3];        // world ranks of this rank's axis lines, by position
   c3d_counters counters_{};
+  std::string poisoned_;
   void* zero_ws_ = nullptr;
   size_t zero_ws_bytes_ = 0;
 };

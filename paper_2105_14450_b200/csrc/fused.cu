@@ -39,6 +39,7 @@ struct EnterArgs {
   uint32_t* peer_entered[2 * kRsMax];    // each peer's op_entered array (mapped)
   const uint32_t* my_entered[2 * kRsMax];  // this rank's flag raised by that peer
   uint32_t* seq;
+  ptx::Fault fault;
 };
 
 // Advances the fused-op epoch and announces this rank's entry to its peers; with
@@ -51,13 +52,14 @@ __global__ void enter_kernel(EnterArgs a) {
   __threadfence_system();
   for (int k = 0; k < a.n; ++k) ptx::st_release_sys(a.peer_entered[k] + a.rank, e);
   if (a.wait)
-    for (int k = 0; k < a.n; ++k) ptx::wait_epoch(a.my_entered[k], e);
+    for (int k = 0; k < a.n; ++k) ptx::wait_epoch(a.my_entered[k], e, a.fault, 0x400u | k);
 }
 
 struct FinishArgs {
   int P, me, grid, done_offset;
   const uint32_t* done[kRsMax];  // this rank's op_done row for source line[k]
   const uint32_t* seq;
+  ptx::Fault fault;
   const char* slots;  // [P][rows*cols] partials (own slot written locally)
   long long slot_elems;
   long long rows, cols;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(256) rs_finish_kernel(const FinishArgs a) {
     int k = i / a.grid;
     const int cta = i - k * a.grid;
     if (k >= a.me) ++k;
-    ptx::wait_epoch(a.done[k] + a.done_offset + cta, epoch);
+    ptx::wait_epoch(a.done[k] + a.done_offset + cta, epoch, a.fault, 0x500u | k);
   }
   __syncthreads();
   const Epilogue& e = a.e;
@@ -183,6 +185,7 @@ void launch_finish(Cube& cube, SymmHeap* h, int axis, int grid, int done_offset,
   fa.grid = grid;
   fa.done_offset = done_offset;
   fa.seq = h->op_seq();
+  fa.fault = h->fault();
   for (int k = 0; k < P; ++k)
     fa.done[k] = h->op_done(cube.rank()) + static_cast<size_t>(line[k]) * kSymmMaxBlocks;
   fa.slots = slots;
@@ -221,6 +224,7 @@ void fill_rs(Cube& cube, SymmHeap* h, int axis, const SymBuf& recv, long long bl
   rs->done_offset = done_offset;
   rs->block_rows = block_rows;
   rs->epoch = h->op_seq();
+  rs->fault = h->fault();
   for (int k = 0; k < P; ++k) {
     rs->dst[k] = (k == me ? recv.local() : recv.at(line[k])) + me * slot_bytes;
     rs->entered[k] = h->op_entered(cube.rank()) + line[k];
@@ -235,6 +239,7 @@ void launch_enter(Cube& cube, SymmHeap* h, const std::vector<int>& peers, bool w
   ea.rank = cube.rank();
   ea.wait = wait ? 1 : 0;
   ea.seq = h->op_seq();
+  ea.fault = h->fault();
   for (int k = 0; k < ea.n; ++k) {
     ea.peer_entered[k] = h->op_entered(peers[k]);
     ea.my_entered[k] = h->op_entered(cube.rank()) + peers[k];

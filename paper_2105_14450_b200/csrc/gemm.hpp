@@ -15,6 +15,8 @@
 
 #include <cstdint>
 
+#include "ptx_fault.hpp"
+
 namespace c3d {
 
 enum DType : int { kF32 = 0, kBF16 = 1 };
@@ -95,6 +97,7 @@ struct RsOut {
   const uint32_t* entered[kRsMax] = {};
   uint32_t* done[kRsMax] = {};
   const uint32_t* epoch = nullptr;
+  Fault fault;  // where a peer that never enters is reported
 };
 
 struct GemmProblem {

@@ -76,6 +76,7 @@ struct TcArgs {
   // fused reduce-scatter (rs_P > 1): block k of the rows goes through rsm.m[k]
   int rs_P, rs_me, rs_block_rows, rs_block0, rs_done_offset;
   const uint32_t* rs_entered[kRsMax];
+  ptx::Fault rs_fault;
   uint32_t* rs_done[kRsMax];
   const uint32_t* rs_epoch;
 };
@@ -674,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           c1 = mrow0 - kr * args.rs_block_rows;
           cmap = &rsm.m[k];
           if (k != args.rs_me && !(entered_mask & (1u << k))) {
-            if (lane == 0) ptx::wait_epoch(args.rs_entered[k], epoch);
+            if (lane == 0) ptx::wait_epoch(args.rs_entered[k], epoch, args.rs_fault, 0x600u | k);
             __syncwarp();
             entered_mask |= 1u << k;
           }
@@ -1117,6 +1118,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     if (!tc_gemm_rs_supported(p, bn)) throw std::runtime_error("tc_gemm: fused reduce-scatter unsupported");
     for (int k = 0; k < p.rs.P; ++k) {
       args.rs_entered[k] = p.rs.entered[k];
+      args.rs_fault = p.rs.fault;
       args.rs_done[k] = p.rs.done[k];
       if (k < p.rs.block0 || k >= p.rs.block0 + p.M / p.rs.block_rows) continue;
       View v;

@@ -8,6 +8,8 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "ptx_fault.hpp"
+
 namespace c3d {
 namespace ptx {
 
@@ -149,18 +151,38 @@ __device__ __forceinline__ uint64_t globaltimer() {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Spins until *f reaches epoch e (wrap-safe). A peer that never arrives traps after
-// 30 s instead of hanging the GPU.
-__device__ inline void wait_epoch(const uint32_t* f, uint32_t e) {
-  if (static_cast<int32_t>(ld_acquire_sys(f) - e) >= 0) return;
+__device__ inline void record_fault(const Fault& ft, uint32_t code, uint32_t site, uint32_t a,
+                                    uint32_t b) {
+  if (!ft.word) return;
+  volatile uint32_t* w = ft.word;
+  if (w[0] != 0u) return;  // keep the first record
+  w[1] = site;
+  w[2] = a;
+  w[3] = b;
+  __threadfence_system();
+  w[0] = code;
+  __threadfence_system();
+}
+
+// Spins until *f reaches epoch e (wrap-safe). A peer that never arrives (or a fault
+// already recorded by another wait) ends the wait with `false` after ft.timeout_ns
+// instead of hanging the GPU; the kernel then finishes with garbage that the host
+// discards (the cube is poisoned and every later call returns C3D_ERR_DESYNC).
+__device__ inline bool wait_epoch(const uint32_t* f, uint32_t e, const Fault& ft, uint32_t site) {
+  if (static_cast<int32_t>(ld_acquire_sys(f) - e) >= 0) return true;
   const uint64_t t0 = globaltimer();
+  uint32_t n = 0;
   while (static_cast<int32_t>(ld_acquire_sys(f) - e) < 0) {
     __nanosleep(32);
-    if (globaltimer() - t0 > 30ull * 1000000000ull) {
-      printf("c3d: timeout waiting for a peer flag (epoch %u, have %u)\n", e, ld_acquire_sys(f));
-      __trap();
+    if ((++n & 255u) == 0u) {
+      if (ft.word && *reinterpret_cast<volatile uint32_t*>(ft.word) != 0u) return false;
+      if (globaltimer() - t0 > ft.timeout_ns) {
+        record_fault(ft, 1u, site, e, ld_acquire_sys(f));
+        return false;
+      }
     }
   }
+  return true;
 }
 
 // ---------------------------------------------------------------- tcgen05

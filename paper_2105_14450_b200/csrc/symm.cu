@@ -30,6 +30,10 @@ struct SymmArgs {
   uint32_t* my_entered;
   uint32_t* my_done;
   uint32_t* my_seq;
+  uint32_t* hdr[kSymmMaxLine];      // header arrays of each position's rank, [src][block]
+  const uint32_t* my_hdr;
+  uint32_t header;                  // (kind, root, op, dtype, count) of this call
+  ptx::Fault fault;
   const char* send;
   char* recv;
   long long count, c0, n, slot_bytes;
@@ -39,8 +43,11 @@ struct SymmArgs {
 using ptx::ld_acquire_sys;
 using ptx::st_release_sys;
 
-__device__ __forceinline__ void wait_epoch(const uint32_t* f, uint32_t e, int /*peer*/) {
-  ptx::wait_epoch(f, e);
+// Fault sites: 0x100 | peer position (entry), 0x200 | peer position (done), 0x300 | peer
+// position (header mismatch).
+__device__ __forceinline__ bool wait_epoch(const SymmArgs& a, const uint32_t* f, uint32_t e,
+                                           uint32_t site) {
+  return ptx::wait_epoch(f, e, a.fault, site);
 }
 
 // 16-byte vector (or scalar) lanes of dtype DT converted to fp32 for reductions.
@@ -108,7 +115,7 @@ __global__ void __launch_bounds__(1024) symm_coll_kernel(const SymmArgs a) {
     const uint32_t e = a.my_seq[q * kSymmMaxBlocks + b] + 1;
     ep[t] = e;
     st_release_sys(a.entered[t] + a.rank * kSymmMaxBlocks + b, e);
-    wait_epoch(a.my_entered + q * kSymmMaxBlocks + b, e, q);
+    wait_epoch(a, a.my_entered + q * kSymmMaxBlocks + b, e, 0x100u | static_cast<uint32_t>(t));
   }
   __syncthreads();
 
@@ -161,9 +168,16 @@ __global__ void __launch_bounds__(1024) symm_coll_kernel(const SymmArgs a) {
   // done: release this block's stores, then wait for the peers' pieces
   if (t < a.P && t != a.me) {
     const int q = a.line[t];
+    // the call's header travels with the done flag (the reference's RoundHeader of kind,
+    // op, length, root and sequence, cube3d/transport.hpp:32-40, 305-319): a peer in a
+    // different collective is a desync, not a silent mix of payloads
+    a.hdr[t][a.rank * kSymmMaxBlocks + b] = a.header;
     __threadfence_system();
     st_release_sys(a.done[t] + a.rank * kSymmMaxBlocks + b, ep[t]);
-    wait_epoch(a.my_done + q * kSymmMaxBlocks + b, ep[t], q);
+    if (wait_epoch(a, a.my_done + q * kSymmMaxBlocks + b, ep[t], 0x200u | static_cast<uint32_t>(t))) {
+      const uint32_t ph = ld_acquire_sys(a.my_hdr + q * kSymmMaxBlocks + b);
+      if (ph != a.header) ptx::record_fault(a.fault, 2u, 0x300u | static_cast<uint32_t>(t), a.header, ph);
+    }
     a.my_seq[q * kSymmMaxBlocks + b] = ep[t];
   }
   __syncthreads();
@@ -212,7 +226,35 @@ void launch(const SymmArgs& a, cudaStream_t s) {
   symm_coll_kernel<DT, VEC><<<a.G, threads, 0, s>>>(a);
 }
 
+// (kind 2 b | root 4 b | max 1 b | dtype 1 b | count 24 b): what every member of the line
+// must agree on for one collective.
+uint32_t coll_header(int op, int root, bool is_max, int dtype, size_t count) {
+  return (static_cast<uint32_t>(op & 3) << 30) | (static_cast<uint32_t>(root & 15) << 26) |
+         (static_cast<uint32_t>(is_max ? 1 : 0) << 25) | (static_cast<uint32_t>(dtype & 1) << 24) |
+         static_cast<uint32_t>(count & 0xFFFFFFu);
+}
+
 }  // namespace
+
+std::string SymmHeap::fault_message() const {
+  if (!fault_host_) return "";
+  volatile uint32_t* w = fault_host_;
+  if (w[0] == 0u) return "";
+  static const char* kinds[] = {"all_gather", "reduce_scatter", "all_reduce", "broadcast"};
+  char buf[256];
+  if (w[0] == 1u) {
+    std::snprintf(buf, sizeof(buf),
+                  "peer did not arrive within the timeout (site 0x%x: expected epoch %u, saw %u)",
+                  w[1], w[2], w[3]);
+  } else {
+    std::snprintf(buf, sizeof(buf),
+                  "collective header mismatch with line position %u: this rank %s count %u, peer "
+                  "%s count %u",
+                  w[1] & 0xFFu, kinds[w[2] >> 30], w[2] & 0xFFFFFFu, kinds[w[3] >> 30],
+                  w[3] & 0xFFFFFFu);
+  }
+  return buf;
+}
 
 SymmHeap::SymmHeap(ncclComm_t world, int world_size, int rank, size_t mailbox_bytes,
                    size_t arena_bytes, cudaStream_t s)
@@ -222,13 +264,18 @@ SymmHeap::SymmHeap(ncclComm_t world, int world_size, int rank, size_t mailbox_by
   mailbox_bytes_ = (mailbox_bytes + 4095) / 4096 * 4096;
   arena_bytes_ = (arena_bytes + 4095) / 4096 * 4096;
   constexpr size_t RB = static_cast<size_t>(kSymmMaxRanks) * kSymmMaxBlocks;
-  // [entered RB][done RB][op_entered R][op_done RB][op_ag RB]
-  flags_bytes_ = ((4 * RB + kSymmMaxRanks) * sizeof(uint32_t) + 4095) / 4096 * 4096;
+  // [entered RB][done RB][op_entered R][op_done RB][op_ag RB][hdr RB]
+  flags_bytes_ = ((5 * RB + kSymmMaxRanks) * sizeof(uint32_t) + 4095) / 4096 * 4096;
   C3D_CUDA(cudaMalloc(&heap_, flags_bytes_ + mailbox_bytes_ + arena_bytes_));
   C3D_CUDA(cudaMemset(heap_, 0, flags_bytes_));
   C3D_CUDA(cudaMalloc(&seq_, (RB + 32) * sizeof(uint32_t)));
   C3D_CUDA(cudaMemset(seq_, 0, (RB + 32) * sizeof(uint32_t)));
   if (arena_bytes_) free_.push_back({0, arena_bytes_});
+  C3D_CUDA(cudaHostAlloc(&fault_host_, 8 * sizeof(uint32_t), cudaHostAllocMapped));
+  std::memset(fault_host_, 0, 8 * sizeof(uint32_t));
+  C3D_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&fault_.word), fault_host_, 0));
+  if (const char* e = std::getenv("C3D_PEER_TIMEOUT_MS"))
+    fault_.timeout_ns = static_cast<unsigned long long>(std::atoll(e)) * 1000000ull;
   C3D_CUDA(cudaDeviceSynchronize());
 
   // exchange IPC handles over the world communicator (the flags are zeroed everywhere
@@ -264,6 +311,7 @@ SymmHeap::SymmHeap(ncclComm_t world, int world_size, int rank, size_t mailbox_by
     op_entered_.push_back(f + 2 * RB);
     op_done_.push_back(f + 2 * RB + kSymmMaxRanks);
     op_ag_.push_back(f + 3 * RB + kSymmMaxRanks);
+    hdr_.push_back(f + 4 * RB + kSymmMaxRanks);
     mbox_.push_back(b + flags_bytes_);
     arena_.push_back(b + flags_bytes_ + mailbox_bytes_);
   }
@@ -274,6 +322,7 @@ SymmHeap::~SymmHeap() {
     if (q != rank_ && q < static_cast<int>(base_.size()) && base_[q]) cudaIpcCloseMemHandle(base_[q]);
   if (heap_) cudaFree(heap_);
   if (seq_) cudaFree(seq_);
+  if (fault_host_) cudaFreeHost(fault_host_);
 }
 
 bool SymmHeap::arena_alloc(size_t bytes, size_t* off) {
@@ -340,6 +389,10 @@ void SymmHeap::all_gather_direct(const std::vector<int>& line, int pos, const vo
   a.my_entered = entered_[rank_];
   a.my_done = done_[rank_];
   a.my_seq = seq_;
+  for (int p = 0; p < P; ++p) a.hdr[p] = hdr_[line[p]];
+  a.my_hdr = hdr_[rank_];
+  a.header = coll_header(kCollAllGather, 0, false, dtype, count);
+  a.fault = fault_;
   a.send = static_cast<const char*>(send);
   a.recv = arena_[rank_] + recv_off;
   a.count = static_cast<long long>(count);
@@ -394,6 +447,10 @@ void SymmHeap::collective(CollOp op, const std::vector<int>& line, int pos, cons
   a.my_entered = entered_[rank_];
   a.my_done = done_[rank_];
   a.my_seq = seq_;
+  for (int p = 0; p < P; ++p) a.hdr[p] = hdr_[line[p]];
+  a.my_hdr = hdr_[rank_];
+  a.header = coll_header(op, root_pos, is_max, dtype, count);
+  a.fault = fault_;
   a.send = static_cast<const char*>(send);
   a.recv = static_cast<char*>(recv);
   a.count = static_cast<long long>(count);

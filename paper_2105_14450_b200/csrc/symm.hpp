@@ -15,8 +15,11 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include "ptx_fault.hpp"
+
 #include <cstddef>
 #include <cstdint>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -67,6 +70,11 @@ class SymmHeap {
   uint32_t* op_ag(int r) const { return op_ag_[r]; }  // gathered-operand arrival, [src][cta]
   uint32_t* op_seq() const { return seq_ + kSymmMaxRanks * kSymmMaxBlocks; }
 
+  // Device-visible fault record of this rank's peer waits (Fault), and its description
+  // ("" while no wait failed).
+  const Fault& fault() const { return fault_; }
+  std::string fault_message() const;
+
   // Symmetric arena: every rank performs the same allocation sequence, so an allocation
   // sits at the same offset in every rank's heap and peers can address it directly.
   // First fit over an address-ordered free list (deterministic). Returns false when full.
@@ -82,7 +90,9 @@ class SymmHeap {
   uint32_t* seq_ = nullptr;  // own per-(peer, block) epoch counters (not shared)
   std::vector<void*> base_;  // mapped heaps (own at rank_)
   std::vector<char*> mbox_;
-  std::vector<uint32_t*> entered_, done_, op_entered_, op_done_, op_ag_;
+  std::vector<uint32_t*> entered_, done_, op_entered_, op_done_, op_ag_, hdr_;
+  uint32_t* fault_host_ = nullptr;
+  Fault fault_;
   std::vector<char*> arena_;
   size_t arena_bytes_ = 0;
   std::vector<std::pair<size_t, size_t>> free_;  // (offset, size), address order

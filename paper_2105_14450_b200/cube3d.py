@@ -401,6 +401,11 @@ class Cube:
     def barrier(self, stream=None):
         call("c3d_cube_barrier", self._h, _stream(stream))
 
+    def check(self, stream=None):
+        """c3d_cube_check: synchronise and raise C3DError("Desync", ...) when a peer wait of
+        this cube failed (timeout or mismatched collective header)."""
+        call("c3d_cube_check", self._h, _stream(stream))
+
     def counters(self) -> dict:
         c = L.c3d_counters()
         call("c3d_counters_get", self._h, C.byref(c))

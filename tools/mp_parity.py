@@ -238,6 +238,45 @@ def loss_check(cube, dims):
     report(f"cross-entropy-f32-{q}ranks", ok, f"loss={losses[0]:.6f} oracle={lo:.6f}")
 
 
+def desync_checks(dims):
+    """Recoverable failures (cube3d/transport.hpp:32-40, 67-78, 305-319): a collective whose
+    members disagree on the length, and a member that never arrives, both surface as
+    C3D_ERR_DESYNC on the affected ranks (no trap, no hang), and the cube stays poisoned."""
+    from paper_2105_14450_b200 import C3DError
+    axis = next((a for a in range(3) if dims[a] > 1), None)
+    if axis is None:
+        return
+    os.environ["C3D_PEER_TIMEOUT_MS"] = "2000"
+    for case in ("header", "timeout"):
+        cube = cdist.make_cube(dims)
+        dev = cube.device_str()
+        pos = cube.coords[axis]
+        names = []
+        try:
+            if case == "header":  # one member gathers 16 more elements than the others
+                n = 1000 + (16 if pos == 1 else 0)
+                cube.all_gather(axis, torch.ones(n, dtype=torch.float32, device=dev))
+            elif pos == 0:  # position 1 never joins this all-gather
+                cube.all_gather(axis, torch.ones(1000, dtype=torch.float32, device=dev))
+            cube.check()
+        except C3DError as e:
+            names.append(e.name)
+        try:  # poisoned: the next call fails too
+            cube.all_reduce(axis, torch.ones(8, dtype=torch.float32, device=dev))
+            cube.check()
+        except C3DError as e:
+            names.append(e.name)
+        got = gather_all((pos, names))
+        dist.barrier()
+        cube.close()
+        if case == "header":
+            ok = all(nm == ["Desync", "Desync"] for _, nm in got)
+        else:  # the waiting members report it; the absent one never waited
+            ok = all((nm == ["Desync", "Desync"]) if p == 0 else True for p, nm in got)
+        report(f"desync-{case}-detected", ok, str(got))
+    os.environ.pop("C3D_PEER_TIMEOUT_MS", None)
+
+
 def main():
     rank, world, local = cdist.init_process_group("nccl")
     torch.cuda.set_device(local)
@@ -254,6 +293,8 @@ def main():
             layer_check(cube, dims, name, c3.BF16, c3.MODE_AUTO)
     cube.close()
     dist.barrier()
+    if os.environ.get("C3D_NCCL_COLL") is None:
+        desync_checks(dims)
     dist.destroy_process_group()
     return 1 if FAILS else 0
 
