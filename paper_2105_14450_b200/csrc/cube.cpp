@@ -68,7 +68,6 @@ Cube::Cube(const int dims[3], int rank, int device, const unsigned char* uid)
 }
 
 Cube::~Cube() {
-  if (zero_ws_) cudaFree(zero_ws_);
   symm_.reset();
   for (auto& c : axis_comm_)
     if (c) ncclCommDestroy(c);
@@ -78,21 +77,6 @@ Cube::~Cube() {
 void Cube::check_fault() {
   if (poisoned_.empty() && symm_) poisoned_ = symm_->fault_message();
   if (!poisoned_.empty()) fail(C3D_ERR_DESYNC, "rank " + std::to_string(rank_) + ": " + poisoned_);
-}
-
-void* Cube::zero_workspace(size_t bytes, cudaStream_t s) {
-  if (bytes <= zero_ws_bytes_) return zero_ws_;
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  C3D_CUDA(cudaStreamIsCapturing(s, &st));
-  if (st != cudaStreamCaptureStatusNone) return nullptr;
-  // outside capture: the old buffer may still be read by work queued on `s`
-  if (zero_ws_) C3D_CUDA(cudaFreeAsync(zero_ws_, s));
-  zero_ws_ = nullptr;
-  zero_ws_bytes_ = 0;
-  C3D_CUDA(cudaMallocAsync(&zero_ws_, bytes, s));
-  C3D_CUDA(cudaMemsetAsync(zero_ws_, 0, bytes, s));
-  zero_ws_bytes_ = bytes;
-  return zero_ws_;
 }
 
 ncclComm_t Cube::comm(int axis) const {

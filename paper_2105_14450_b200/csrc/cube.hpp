@@ -115,11 +115,6 @@ class Cube {
   // the reference poisons a group whose collective failed (cube3d/transport.hpp:67-78).
   void check_fault();
 
-  // Persistent device workspace that is all-zero between uses (kernels that use it
-  // restore the zeros, e.g. the flash backward's fp32 dQ accumulator). Grows on demand
-  // outside stream capture; returns nullptr when it would have to grow while `s` is
-  // being captured (the caller then uses a stream-ordered buffer of its own).
-  void* zero_workspace(size_t bytes, cudaStream_t s);
   void reset_counters() { std::memset(&counters_, 0, sizeof(counters_)); }
 
  private:
@@ -137,8 +132,6 @@ class Cube {
   std::vector<int> line_[3];        // world ranks of this rank's axis lines, by position
   c3d_counters counters_{};
   std::string poisoned_;
-  void* zero_ws_ = nullptr;
-  size_t zero_ws_bytes_ = 0;
 };
 
 }  // namespace c3d

@@ -143,71 +143,6 @@ void prof_end(cudaStream_t s, void* token, int tag, double bytes) {
   pr.recs.push_back(rec);
 }
 
-bool& skip_prof() {
-  static thread_local bool skip = false;
-  return skip;
-}
-
-// Column sums of a bf16 [rows][cols] matrix on the tensor cores: C[c][n] =
-// sum_r x[r][c] * 1 with a 64-wide block of ones as the B operand (x read once, fp32
-// accumulation in a fixed order, so the result is deterministic), column 0 kept.
-bool colsum_tc(const void* x, int64_t rows, int64_t cols, float* out, cudaStream_t s) {
-  if (std::getenv("C3D_NO_COLSUM_TC")) return false;
-  if (rows < 64 || rows % 64 || cols % 64 || reinterpret_cast<uintptr_t>(x) % 16) return false;
-  static std::mutex mu;
-  static void* ones = nullptr;
-  static int64_t ones_rows = 0;
-  static int num_sms = 0;
-  {
-    std::lock_guard<std::mutex> g(mu);
-    if (ones_rows < rows) {
-      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-      C3D_CUDA(cudaStreamIsCapturing(s, &st));
-      if (st != cudaStreamCaptureStatusNone) return false;  // no allocation inside a capture
-      if (ones) C3D_CUDA(cudaFree(ones));
-      const int64_t n = 64 * rows;
-      C3D_CUDA(cudaMalloc(&ones, n * 2));
-      std::vector<uint16_t> h(static_cast<size_t>(n), 0x3F80);  // bf16 1.0
-      C3D_CUDA(cudaMemcpy(ones, h.data(), n * 2, cudaMemcpyHostToDevice));
-      ones_rows = rows;
-    }
-    if (!num_sms) {
-      int dev = 0;
-      C3D_CUDA(cudaGetDevice(&dev));
-      C3D_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-  }
-  GemmProblem p;
-  p.M = cols;
-  p.N = 64;
-  p.K = rows;
-  p.a.base = const_cast<void*>(x);
-  p.a.dtype = kBF16;
-  p.a.sr = 1;
-  p.a.sc = cols;
-  p.b.base = ones;
-  p.b.dtype = kBF16;
-  p.b.sr = ones_rows;
-  p.b.sc = 1;
-  float* tmp = nullptr;
-  C3D_CUDA(cudaMallocAsync(&tmp, sizeof(float) * cols * 64, s));
-  p.epi.out.base = tmp;
-  p.epi.out.dtype = kF32;
-  p.epi.out.sr = 64;
-  const int bn = tc_pick_bn(p.M, p.N, 1, num_sms);
-  if (!tc_gemm_supported(p, bn)) {
-    C3D_CUDA(cudaFreeAsync(tmp, s));
-    return false;
-  }
-  skip_prof() = true;  // not a product of the layer: kept out of the GEMM roofline
-  run_gemm(p, C3D_MODE_TC, num_sms, s);
-  skip_prof() = false;
-  C3D_CUDA(cudaMemcpy2DAsync(out, sizeof(float), tmp, 64 * sizeof(float), sizeof(float), cols,
-                             cudaMemcpyDeviceToDevice, s));
-  C3D_CUDA(cudaFreeAsync(tmp, s));
-  return true;
-}
-
 void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s) {
   if (p.M == 0 || p.N == 0 || p.batch == 0) return;
   const bool bf16_ops = p.a.dtype == kBF16 && p.b.dtype == kBF16;
@@ -216,7 +151,7 @@ void run_gemm(const GemmProblem& p, int mode, int num_sms, cudaStream_t s) {
     if (tc_gemm_supported(p, bn)) {
       Profiler& pr = prof();
       ProfRec rec{};
-      const bool on = pr.enabled && !skip_prof();
+      const bool on = pr.enabled;
       if (on) {
         std::lock_guard<std::mutex> g(pr.mu);
         rec.start = pr.take();

@@ -125,17 +125,28 @@ __global__ void colsum_partial_kernel(const void* x, int xdt, const void* y, int
   }
   partial[blockIdx.y * cols + c] = acc;
 }
-// Vector form: 8 consecutive columns per thread (16-B loads), rows unrolled by 4.
-template <int XDT, int YDT>
-__global__ void colsum_partial_vec_kernel(const void* x, const void* y, int64_t rows, int64_t cols,
-                                          float* partial) {
-  const int64_t c8 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) * 8;
-  if (c8 >= cols) return;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kColChunkRows;
-  const int64_t r1 = min(rows, r0 + kColChunkRows);
+// Column sums at HBM speed: a CTA of 8 warps covers 256 columns (8 per lane, 16-B loads)
+// x 128 rows (16 per warp, all loads of a warp issued before they are summed), so 4-8
+// resident CTAs keep >= 64 KB per SM in flight. Warps combine through shared memory in a
+// fixed order into a per-chunk partial; the last CTA of each column tile (counter) sums
+// the chunks in chunk order -- deterministic, and no second launch. With DUAL, one pass
+// over x yields both colsum(x * y) (out) and colsum(x) (out2): LayerNorm's dgamma and
+// dbeta.
+constexpr int kCsRows = 128, kCsWarpRows = 16;
+template <int XDT, int YDT, bool DUAL>
+__global__ void __launch_bounds__(256) colsum_chunk_kernel(const void* x, const void* y, int64_t rows,
+                                                           int64_t cols, float* partial,
+                                                           unsigned* counters, float* out,
+                                                           float* out2) {
+  constexpr int NS = DUAL ? 2 : 1;
+  __shared__ float red[NS][8][256];
+  __shared__ unsigned last;
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int64_t c8 = blockIdx.x * 256LL + lane * 8;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kCsRows + w * kCsWarpRows;
   auto load8 = [&](const void* base, int dt, int64_t off, float (&v)[8]) {
     if (dt == kBF16) {
-      const uint4 q = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off);
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off));
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -144,66 +155,117 @@ __global__ void colsum_partial_vec_kernel(const void* x, const void* y, int64_t 
         v[2 * i + 1] = f.y;
       }
     } else {
-      const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
-      const float4 b = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4);
+      const float4 a = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4));
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
       v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     }
   };
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    float v[4][8];
+  float acc[NS][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load8(x, XDT, (r + u) * cols + c8, v[u]);
-    if (YDT >= 0) {
-      float w[4][8];
+  for (int k = 0; k < NS; ++k)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load8(y, YDT, (r + u) * cols + c8, w[u]);
+    for (int i = 0; i < 8; ++i) acc[k][i] = 0.f;
+  if (c8 < cols) {
+    constexpr int U = YDT >= 0 ? 4 : 8;  // loads in flight per operand
+#pragma unroll 1
+    for (int k0 = 0; k0 < kCsWarpRows; k0 += U) {
+      float v[U][8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = r0 + k0 + u;
+        if (r < rows) load8(x, XDT, r * cols + c8, v[u]);
+        else
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[u][i] *= w[u][i];
+          for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+      }
+      if (YDT >= 0) {
+        float g[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t r = r0 + k0 + u;
+          if (r < rows) load8(y, YDT, r * cols + c8, g[u]);
+          else
+#pragma unroll
+            for (int i = 0; i < 8; ++i) g[u][i] = 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (DUAL) acc[1][i] += v[u][i];
+            v[u][i] *= g[u][i];
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += v[u][i];
   }
-  for (; r < r1; ++r) {
-    float v[8];
-    load8(x, XDT, r * cols + c8, v);
-    if (YDT >= 0) {
-      float w[8];
-      load8(y, YDT, r * cols + c8, w);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] *= w[i];
-    }
+  for (int k = 0; k < NS; ++k)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] += v[i];
-  }
-  float* out = partial + blockIdx.y * cols + c8;
-  reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-  reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
-}
-
-// Second stage over many chunks: 8 warps split the chunks of 32 columns, partials merged
-// in a fixed order through shared memory (deterministic).
-__global__ void colsum_final_wide_kernel(const float* partial, int64_t chunks, int64_t cols,
-                                         float* out) {
-  __shared__ float red[8][32];
-  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
-  const int64_t c = blockIdx.x * 32LL + lane;
-  float acc = 0.f;
-  if (c < cols)
-    for (int64_t k = w; k < chunks; k += 8) acc += partial[k * cols + c];
-  red[w][lane] = acc;
+    for (int i = 0; i < 8; ++i) red[k][w][lane * 8 + i] = acc[k][i];
   __syncthreads();
-  if (w == 0 && c < cols) {
-    float t = 0.f;
+  const int64_t c = blockIdx.x * 256LL + threadIdx.x;
+  const int64_t nchunks = gridDim.y;
+  if (c < cols) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t += red[i][lane];
-    out[c] = t;
+    for (int k = 0; k < NS; ++k) {
+      float t = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += red[k][q][threadIdx.x];
+      partial[(k * nchunks + blockIdx.y) * cols + c] = t;
+    }
+  }
+  // the last chunk CTA of this column tile reduces the tile's chunks in order
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counters + blockIdx.x, 1u);
+    last = prev + 1 == static_cast<unsigned>(nchunks) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // warp w sums chunks w, w + 8, ... (8 columns per lane, 4 chunks in flight), then the
+  // warps combine in order: a fixed association, so the result is deterministic
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c8 < cols) {
+      const float* base = partial + k * nchunks * cols + c8;
+#pragma unroll 1
+      for (int64_t q0 = w; q0 < nchunks; q0 += 32) {
+        float4 v[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t q = q0 + 8 * u;
+          if (q < nchunks) {
+            v[u][0] = __ldcg(reinterpret_cast<const float4*>(base + q * cols));
+            v[u][1] = __ldcg(reinterpret_cast<const float4*>(base + q * cols + 4));
+          } else {
+            v[u][0] = v[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          t[0] += v[u][0].x; t[1] += v[u][0].y; t[2] += v[u][0].z; t[3] += v[u][0].w;
+          t[4] += v[u][1].x; t[5] += v[u][1].y; t[6] += v[u][1].z; t[7] += v[u][1].w;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[0][w][lane * 8 + i] = t[i];
+    __syncthreads();
+    if (c < cols) {
+      float sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += red[0][q][threadIdx.x];
+      (k == 0 ? out : out2)[c] = sum;
+    }
   }
 }
 
@@ -583,43 +645,64 @@ void k_apply_epilogue(const void* in, int in_dtype, int64_t rows, int64_t cols,
   check_launch("apply_epilogue");
 }
 
-bool colsum_tc(const void* x, int64_t rows, int64_t cols, float* out, cudaStream_t s);
 
 void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int64_t cols,
-              float* out, cudaStream_t s) {
+              float* out, cudaStream_t s, float* out_x) {
   if (cols == 0) return;
-  if (!y && xdt == kBF16 && colsum_tc(x, rows, cols, out, s)) return;
-  const int64_t chunks = std::max<int64_t>(1, (rows + kColChunkRows - 1) / kColChunkRows);
-  float* partial = nullptr;
-  C3D_CUDA(cudaMallocAsync(&partial, chunks * cols * sizeof(float), s));
-  dim3 g1(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(chunks));
-  if (rows == 0) {
-    C3D_CUDA(cudaMemsetAsync(partial, 0, chunks * cols * sizeof(float), s));
-  } else {
-    auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
-    const bool vec = cols % 8 == 0 && al(x) && (!y || al(y));
-    if (vec) {
-      dim3 gv(static_cast<unsigned>((cols / 8 + 127) / 128), static_cast<unsigned>(chunks));
-      const int yk = y ? ydt : -1;
-      if (xdt == kBF16 && yk == -1) colsum_partial_vec_kernel<kBF16, -1><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-      else if (xdt == kBF16 && yk == kBF16) colsum_partial_vec_kernel<kBF16, kBF16><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-      else if (xdt == kBF16 && yk == kF32) colsum_partial_vec_kernel<kBF16, kF32><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-      else if (xdt == kF32 && yk == -1) colsum_partial_vec_kernel<kF32, -1><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-      else if (xdt == kF32 && yk == kBF16) colsum_partial_vec_kernel<kF32, kBF16><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-      else colsum_partial_vec_kernel<kF32, kF32><<<gv, 128, 0, s>>>(x, y, rows, cols, partial);
-    } else {
-      colsum_partial_kernel<<<g1, 128, 0, s>>>(x, xdt, y, ydt, rows, cols, partial);
+  auto al = [](const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; };
+  const bool vec = cols % 8 == 0 && al(x) && (!y || al(y)) && rows > 0;
+  if (!vec) {
+    // generic path: two-stage partial / final kernels (and a second pass for out_x)
+    const int64_t chunks = std::max<int64_t>(1, (rows + kColChunkRows - 1) / kColChunkRows);
+    float* partial = nullptr;
+    C3D_CUDA(cudaMallocAsync(&partial, chunks * cols * sizeof(float), s));
+    for (int pass = 0; pass < (out_x && y ? 2 : 1); ++pass) {
+      const void* yy = pass == 0 ? y : nullptr;
+      float* o = pass == 0 ? out : out_x;
+      if (rows == 0) {
+        C3D_CUDA(cudaMemsetAsync(partial, 0, chunks * cols * sizeof(float), s));
+      } else {
+        dim3 g1(static_cast<unsigned>((cols + 127) / 128), static_cast<unsigned>(chunks));
+        colsum_partial_kernel<<<g1, 128, 0, s>>>(x, xdt, yy, ydt, rows, cols, partial);
+        check_launch("colsum_partial");
+      }
+      colsum_final_kernel<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, s>>>(partial, chunks,
+                                                                                    cols, o);
+      check_launch("colsum_final");
     }
-    check_launch("colsum_partial");
+    C3D_CUDA(cudaFreeAsync(partial, s));
+    return;
   }
-  if (chunks >= 32)
-    colsum_final_wide_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(partial, chunks,
-                                                                                   cols, out);
-  else
-    colsum_final_kernel<<<static_cast<unsigned>((cols + 127) / 128), 128, 0, s>>>(partial, chunks,
-                                                                                  cols, out);
-  check_launch("colsum_final");
-  C3D_CUDA(cudaFreeAsync(partial, s));
+  const bool dual = out_x && y;
+  const int64_t chunks = (rows + kCsRows - 1) / kCsRows;
+  const int64_t tiles = (cols + 255) / 256;
+  char* scratch = nullptr;
+  const size_t pbytes = static_cast<size_t>((dual ? 2 : 1) * chunks * cols) * sizeof(float);
+  C3D_CUDA(cudaMallocAsync(&scratch, pbytes + tiles * sizeof(unsigned), s));
+  unsigned* counters = reinterpret_cast<unsigned*>(scratch + pbytes);
+  C3D_CUDA(cudaMemsetAsync(counters, 0, tiles * sizeof(unsigned), s));
+  float* partial = reinterpret_cast<float*>(scratch);
+  dim3 g(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
+  const int yk = y ? ydt : -1;
+#define C3D_COLSUM(XD, YD, DU) \
+  colsum_chunk_kernel<XD, YD, DU><<<g, 256, 0, s>>>(x, y, rows, cols, partial, counters, out, out_x)
+  if (dual) {
+    if (xdt == kBF16 && yk == kBF16) C3D_COLSUM(kBF16, kBF16, true);
+    else if (xdt == kBF16) C3D_COLSUM(kBF16, kF32, true);
+    else if (yk == kBF16) C3D_COLSUM(kF32, kBF16, true);
+    else C3D_COLSUM(kF32, kF32, true);
+  } else {
+    if (xdt == kBF16 && yk == -1) C3D_COLSUM(kBF16, -1, false);
+    else if (xdt == kBF16 && yk == kBF16) C3D_COLSUM(kBF16, kBF16, false);
+    else if (xdt == kBF16 && yk == kF32) C3D_COLSUM(kBF16, kF32, false);
+    else if (xdt == kF32 && yk == -1) C3D_COLSUM(kF32, -1, false);
+    else if (xdt == kF32 && yk == kBF16) C3D_COLSUM(kF32, kBF16, false);
+    else C3D_COLSUM(kF32, kF32, false);
+  }
+#undef C3D_COLSUM
+  check_launch("colsum_chunk");
+  if (out_x && !y) C3D_CUDA(cudaMemcpyAsync(out_x, out, cols * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  C3D_CUDA(cudaFreeAsync(scratch, s));
 }
 
 void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s) {

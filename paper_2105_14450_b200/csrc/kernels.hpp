@@ -17,10 +17,11 @@ namespace c3d {
 void k_apply_epilogue(const void* in, int in_dtype, int64_t rows, int64_t cols,
                       const Epilogue& e, cudaStream_t s);
 
-// out[c] = sum_r x[r][c] (* y[r][c] if y), fp32, deterministic order.
+// out[c] = sum_r x[r][c] (* y[r][c] if y), fp32, deterministic order; with out_x also
+// out_x[c] = sum_r x[r][c] from the same pass (LayerNorm dgamma and dbeta together).
 // add_vec_bwd colsum (cube3d/ops3d.hpp:365-367), mul_vec_bwd (:408-413), LN dbeta/dgamma.
 void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int64_t cols,
-              float* out, cudaStream_t s);
+              float* out, cudaStream_t s, float* out_x = nullptr);
 
 void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
 // y = gelu(x), x <- gelu'(x) (n elements, in place on x).

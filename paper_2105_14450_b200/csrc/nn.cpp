@@ -218,12 +218,11 @@ void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const 
   const Dirs d = triple_for_group(dy.group);
   const float inv_h = 1.f / static_cast<float>(dy.hidden);
   if (sink) {
-    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, sink, s);
-    k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, sink + dy.cols, s);
+    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, sink, s, sink + dy.cols);
   } else if (dgamma && dbeta) {  // collective on every rank (see linear_bwd)
     DevBuf cs(static_cast<size_t>(2 * dy.cols) * sizeof(float), s);
-    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, cs.as<float>(), s);
-    k_colsum(dy.data, dy.dtype, nullptr, kF32, dy.rows, dy.cols, cs.as<float>() + dy.cols, s);
+    k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, cs.as<float>(), s,
+             cs.as<float>() + dy.cols);
     Vec outs[2] = {*dgamma, *dbeta};
     outs[0].len = outs[1].len = dy.hidden;
     reduce_to_diagonal(cube, d, cs.as<float>(), 2, outs, s);
