@@ -342,6 +342,74 @@ def fp32_mode_figure(cube, wl, steps=3):
             "dtype": "f32", "path": "MODE_F32: fp32 storage, SIMT fp32 GEMMs, eager"}
 
 
+# ---------------------------------------------------- cfg4 training step (extra)
+def cfg4_figure(cube, steps=2, layers=24, vocab=32768):
+    """BASELINE.json configs[3]: a 24-layer 3-D Transformer stack, hidden 2048, seq 1024,
+    16 heads (dh = 128, flash kernels), with a 3-D cross-entropy head over a 32768-token
+    vocabulary: one training step = stack fwd + loss fwd/bwd + stack bwd, bf16, eager,
+    CUDA events, max over ranks. The configured batch is 64; the largest of 64 / 32 / 16
+    that fits the GPUs' memory is used and reported. A labelled extra figure."""
+    import torch
+    from paper_2105_14450_b200 import C3DError
+    from paper_2105_14450_b200 import cube3d as c3
+    from paper_2105_14450_b200 import dist
+    s, n, h = 1024, 16, 2048
+    last_err = None
+    for b in (64, 32, 16):
+        if b % cube.dims[0]:
+            continue
+        try:
+            wl = dict(b=b, s=s, n=n, h=h)
+            cfg = c3.TransformerConfig(b, s, n, h)
+            plist = [make_layer_inputs(cube, wl, c3.BF16)[0] for _ in range(layers)]
+            _, x, _ = make_layer_inputs(cube, wl, c3.BF16)
+            dev = cube.device_str()
+            d0 = c3.triple_for_group(0)
+            gen = torch.Generator(device=dev).manual_seed(77)
+            wsh = cube.local_shape(c3.WEIGHT, h, vocab, d0)
+            head = c3.LinearParams(
+                c3.ShardedMatrix((torch.rand(wsh, device=dev, generator=gen) * 0.04 - 0.02)
+                                 .to(torch.bfloat16), h, vocab, c3.WEIGHT, d0),
+                c3.DiagonalVector(torch.zeros(cube.diag_len(vocab), device=dev), vocab), 0)
+            targets = torch.randint(0, vocab, (b * s,), device=dev, generator=gen,
+                                    dtype=torch.int32)
+
+            def step():
+                y, sv = c3.transformer_stack_fwd(cube, x, plist, cfg, c3.GroupState(0))
+                loss, lsv = c3.cross_entropy_fwd(cube, y, head, targets, c3.GroupState(0))
+                dyl, _, _ = c3.cross_entropy_bwd(cube, lsv, head)
+                c3.transformer_stack_bwd(cube, dyl, sv, plist, cfg, grad_dtype=c3.F32)
+                return loss
+
+            step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            cube.reset_counters()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                loss = step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = dist.max_over_ranks(e0.elapsed_time(e1) / steps)
+            flops = 2.0 * dist.sum_over_ranks(float(cube.counters()["multiply_adds"])) / steps
+            mem = torch.cuda.max_memory_allocated() / 2 ** 30
+            del plist, x, head, targets
+            return {"workload": f"cfg4: {layers}-layer stack, hidden {h}, seq {s}, {n} heads, "
+                                f"batch {b}, cross-entropy over {vocab} tokens",
+                    "batch": b, "seq_per_s": b / (ms * 1e-3), "tokens_per_s": b * s / (ms * 1e-3),
+                    "ms_per_step": ms, "steps": steps, "tflops": flops / (ms * 1e-3) / 1e12,
+                    "loss": float(loss.item()), "max_mem_gib_torch": mem,
+                    "dtype": "bf16 (fp32 accumulate, fp32 logits)", "timing": "eager, CUDA events"}
+        except (torch.OutOfMemoryError, C3DError) as ex:
+            last_err = str(ex)[:200]
+            import gc
+            gc.collect()
+            torch.cuda.empty_cache()
+            continue
+    return {"error": last_err}
+
+
 # -------------------------------------------------------------------- our arm
 def make_layer_inputs(cube, wl, dtype):
     import torch
@@ -532,6 +600,13 @@ def our_arm(args, wl):
                       "note": "max(flops / (bf16 peak x GPUs), elements sent per rank "
                               "x 2 B / 770 GB/s) / measured ms; HBM-bound kernels not included"}
 
+    cfg4 = None
+    if not args.no_cfg4:
+        try:
+            cfg4 = cfg4_figure(cube)
+        except Exception as ex:  # report, never fake
+            cfg4 = {"error": str(ex)[:300]}
+
     f32 = None
     if not args.no_fp32:
         try:
@@ -578,6 +653,7 @@ def our_arm(args, wl):
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
             "layer_roofline": layer_roofline,
             "fp32_mode": f32,
+            "cfg4_training_step": cfg4,
             "collectives": {"calls_per_step": comm_n / prof_steps,
                             "ms_per_step": comm_ms / prof_steps,
                             "payload_mb_per_step": comm_bytes / prof_steps / 1e6,
@@ -621,6 +697,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-exact mode figure")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the cfg4 training-step figure")
     ap.add_argument("--no-matmul", action="store_true", help="skip the 3-D matmul TFLOP/s line")
     ap.add_argument("--grid", default=None,
                     help="px x py x pz (e.g. 4x1x1); default: 1x1x1, 2x1x1, 1x2x2, 2x2x2")
