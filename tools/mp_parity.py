@@ -123,6 +123,19 @@ def matmul_checks(cube, dims):
     report("add_vec-fwd-bwd", O.rel_err(got, am + vec) < 1e-6 and O.rel_err(gdb, am.sum(0)) < 1e-5)
 
 
+def traffic_check(cube, dims, tag, b, s, n, h, bf16, which):
+    """Zero unaccounted traffic (cube3d/verify.hpp:671-682): the elements all ranks sent
+    during one layer forward (which=0) or backward (1) equal the library's closed-form
+    model (paper_2105_14450_b200/traffic.py), and sent == received."""
+    from paper_2105_14450_b200 import traffic as T
+    cnt = gather_all(cube.counters())
+    sent = sum(c["elements_sent"] for c in cnt)
+    recv = sum(c["elements_received"] for c in cnt)
+    want = T.layer_traffic(b, s, n, h, dims, flash=T.flash_applies(s, n, h, dims, bf16))[which]
+    report(f"traffic-model-{tag}", sent == want and sent == recv,
+           f"measured {sent} (received {recv}), model {want}")
+
+
 def layer_check(cube, dims, name, dtype, mode):
     d = golden(name)
     _, b, s, n, h, seed = (int(v) for v in d["cfg"])
@@ -138,8 +151,14 @@ def layer_check(cube, dims, name, dtype, mode):
     gs = c3.GroupState(0)
     cube.reset_counters()
     y, saved = c3.transformer_layer_fwd(cube, X, params, cfg, gs, mode)
+    torch.cuda.synchronize()
+    traffic_check(cube, dims, f"{name}-{'f32' if dtype == c3.F32 else 'bf16'}-fwd", b, s, n, h,
+                  dtype == c3.BF16, 0)
+    cube.reset_counters()
     dx, grads = c3.transformer_layer_bwd(cube, DY, saved, params, cfg, mode, grad_dtype=c3.F32)
     torch.cuda.synchronize()
+    traffic_check(cube, dims, f"{name}-{'f32' if dtype == c3.F32 else 'bf16'}-bwd", b, s, n, h,
+                  dtype == c3.BF16, 1)
     Y = c3.activation_to_global(gather_all(to_np(y.local)), b, s, h, 0, dims)
     DX = c3.activation_to_global(gather_all(to_np(dx.local)), b, s, h, 0, dims)
     G = {}
@@ -166,15 +185,10 @@ def layer_check(cube, dims, name, dtype, mode):
     worst = max(errs, key=errs.get)
     report(f"layer-{name}-{'f32' if dtype == c3.F32 else 'bf16'}", ok,
            f"worst {worst}={errs[worst]:.2e}")
-    # traffic: elements moved by all ranks (sent == received, cube3d/counters.hpp:32-36)
-    cnt = gather_all(cube.counters())
-    sent = sum(c["elements_sent"] for c in cnt)
-    recv = sum(c["elements_received"] for c in cnt)
-    report(f"layer-{name}-traffic-balanced", sent == recv, f"sent={sent} recv={recv}")
 
 
 def layer_tc_check(cube, dims):
-    """bf16 layer at a shape that takes the fused tcgen05 attention kernels (dh = 64,
+    """bf16 layer at a shape that takes the flash tcgen05 attention kernels (dh = 64,
     256 / 512 keys per rank; with the seq axis split, the distributed-softmax passes)
     against the fp64 oracle on the same bf16-rounded inputs."""
     b, s, n, h = 2, 512, 8, 512
@@ -187,9 +201,14 @@ def layer_tc_check(cube, dims):
     params = c3.partition_layer_params(cube, gp, 0, c3.BF16)
     X = c3.activation_to_device(cube, x, b, s, 0, c3.BF16)
     DY = c3.activation_to_device(cube, dy, b, s, 0, c3.BF16)
+    cube.reset_counters()
     y, saved = c3.transformer_layer_fwd(cube, X, params, cfg, c3.GroupState(0))
+    torch.cuda.synchronize()
+    traffic_check(cube, dims, "flash-shape-fwd", b, s, n, h, True, 0)
+    cube.reset_counters()
     dx, grads = c3.transformer_layer_bwd(cube, DY, saved, params, cfg, grad_dtype=c3.F32)
     torch.cuda.synchronize()
+    traffic_check(cube, dims, "flash-shape-bwd", b, s, n, h, True, 1)
     Y = c3.activation_to_global(gather_all(to_np(y.local)), b, s, h, 0, dims)
     DX = c3.activation_to_global(gather_all(to_np(dx.local)), b, s, h, 0, dims)
     PO = O.LayerParams(**{f: getattr(gp, f) for f in O.FIELDS})
