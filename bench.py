@@ -211,9 +211,42 @@ def matmul_tflops(cube, n=8192, iters=20):
     e1.record()
     torch.cuda.synchronize()
     ms = dist.max_over_ranks(e0.elapsed_time(e1) / iters)
-    return {"m_n_k": n, "tflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e12, "ms": ms,
-            "grid": "x".join(map(str, cube.dims)), "dtype": "bf16 (fp32 accumulate)",
-            "path": "c3d_matmul_ab_fwd: all-gathers + tcgen05 GEMM + fused reduce-scatter"}
+    out = {"m_n_k": n, "tflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e12, "ms": ms,
+           "grid": "x".join(map(str, cube.dims)), "dtype": "bf16 (fp32 accumulate)",
+           "path": "c3d_matmul_ab_fwd: all-gathers + tcgen05 GEMM + fused reduce-scatter"}
+    del gr
+    # the 1-D row-partition baseline of configs[4] on the same GPUs (baselines.py)
+    world = cube.dims[0] * cube.dims[1] * cube.dims[2]
+    try:
+        from paper_2105_14450_b200.baselines import OneDMatmul
+        line = cube if cube.dims == (world, 1, 1) else dist.make_cube((world, 1, 1))
+        od = OneDMatmul(line, n)
+        for _ in range(3):
+            od.step()
+        torch.cuda.synchronize()
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            for _ in range(iters):
+                od.step()
+        g1.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        g1.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms1 = dist.max_over_ranks(e0.elapsed_time(e1) / iters)
+        out["one_d_baseline"] = {"tflops": od.flops() / (ms1 * 1e-3) / 1e12, "ms": ms1,
+                                 "grid": f"{world}x1x1",
+                                 "path": "1-D row partition: all-gather B + tcgen05 GEMM"}
+        del g1, od
+        if line is not cube:
+            torch.cuda.synchronize()
+            dist.barrier()
+            line.close()
+    except Exception as ex:  # report, never fake
+        out["one_d_baseline"] = {"error": str(ex)[:200]}
+    return out
 
 
 # ------------------------------------------------------------ end-to-end arm

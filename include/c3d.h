@@ -252,6 +252,25 @@ int c3d_matmul_atb_fwd(c3d_cube* cube, int mode, const c3d_matrix* a, const c3d_
 int c3d_matmul_atb_bwd(c3d_cube* cube, int mode, const c3d_matrix* dc, const c3d_matrix* a,
                        const c3d_matrix* b, c3d_matrix* da, c3d_matrix* db, void* stream);
 
+/* Batched 3-D matmuls (cube3d/ops3d.hpp:418-494, BatchedShardedMatrix): `na` slices of A,
+ * `nb` of B (and `ndc` of dC), one full 3-D product per slice in order -- the counters equal
+ * the looped accounting. Different extents: C3D_ERR_BATCH_MISMATCH before any work. */
+int c3d_batched_matmul_ab_fwd(c3d_cube* cube, int mode, int na, const c3d_matrix* a, int nb,
+                              const c3d_matrix* b, c3d_matrix* c, void* stream);
+int c3d_batched_matmul_abt_fwd(c3d_cube* cube, int mode, int na, const c3d_matrix* a, int nb,
+                               const c3d_matrix* b, c3d_matrix* c, void* stream);
+int c3d_batched_matmul_atb_fwd(c3d_cube* cube, int mode, int na, const c3d_matrix* a, int nb,
+                               const c3d_matrix* b, c3d_matrix* c, void* stream);
+int c3d_batched_matmul_ab_bwd(c3d_cube* cube, int mode, int ndc, const c3d_matrix* dc, int na,
+                              const c3d_matrix* a, int nb, const c3d_matrix* b, c3d_matrix* da,
+                              c3d_matrix* db, void* stream);
+int c3d_batched_matmul_abt_bwd(c3d_cube* cube, int mode, int ndc, const c3d_matrix* dc, int na,
+                               const c3d_matrix* a, int nb, const c3d_matrix* b, c3d_matrix* da,
+                               c3d_matrix* db, void* stream);
+int c3d_batched_matmul_atb_bwd(c3d_cube* cube, int mode, int ndc, const c3d_matrix* dc, int na,
+                               const c3d_matrix* a, int nb, const c3d_matrix* b, c3d_matrix* da,
+                               c3d_matrix* db, void* stream);
+
 /* ---------------------------------------------------------- vector ops */
 /* add_vec_fwd/bwd (cube3d/ops3d.hpp:347-372): C = A + b rowwise; db = colsum(dC)
  * reduced onto the diagonal ranks (reduce_to_diagonal, :315-336). */

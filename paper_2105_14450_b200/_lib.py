@@ -113,6 +113,13 @@ SIGNATURES = {
     "c3d_gemm": [C.c_int64, C.c_int64, C.c_int64, C.c_int, P(c3d_view), P(c3d_view),
                  P(c3d_view), C.c_float, VP, C.c_int, C.c_int, C.c_int, VP],
     "c3d_matmul_ab_fwd": [VP, C.c_int, P(c3d_matrix), P(c3d_matrix), P(c3d_matrix), VP],
+    **{f"c3d_batched_matmul_{k}_fwd": [VP, C.c_int, C.c_int, P(c3d_matrix), C.c_int,
+                                       P(c3d_matrix), P(c3d_matrix), VP]
+       for k in ("ab", "abt", "atb")},
+    **{f"c3d_batched_matmul_{k}_bwd": [VP, C.c_int, C.c_int, P(c3d_matrix), C.c_int,
+                                       P(c3d_matrix), C.c_int, P(c3d_matrix), P(c3d_matrix),
+                                       P(c3d_matrix), VP]
+       for k in ("ab", "abt", "atb")},
     "c3d_matmul_ab_bwd": [VP, C.c_int, P(c3d_matrix), P(c3d_matrix), P(c3d_matrix),
                           P(c3d_matrix), P(c3d_matrix), VP],
     "c3d_matmul_abt_fwd": [VP, C.c_int, P(c3d_matrix), P(c3d_matrix), P(c3d_matrix), VP],

@@ -484,6 +484,55 @@ C3D_MATMUL_BWD(matmul_ab_bwd)
 C3D_MATMUL_BWD(matmul_abt_bwd)
 C3D_MATMUL_BWD(matmul_atb_bwd)
 
+// Batched variants (cube3d/ops3d.hpp:418-494): one full 3-D matmul per slice, in order,
+// so the counters equal the looped accounting; extents that differ are BatchMismatch
+// before anything is enqueued (ops3d.hpp:432-437).
+namespace {
+void require_same_batch(int na, int nb) {
+  if (na != nb)
+    c3d::fail(C3D_ERR_BATCH_MISMATCH,
+              "batch extents differ: " + std::to_string(na) + " vs " + std::to_string(nb));
+  if (na < 0) c3d::fail(C3D_ERR_CONFIG_INVALID, "negative batch extent");
+}
+}  // namespace
+#define C3D_BATCHED_FWD(name)                                                                   \
+  int c3d_batched_##name(c3d_cube* cube, int mode, int na, const c3d_matrix* a, int nb,         \
+                         const c3d_matrix* b, c3d_matrix* c, void* stream) {                    \
+    return guard([&] {                                                                          \
+      require_same_batch(na, nb);                                                               \
+      auto& cb = get(cube);                                                                     \
+      for (int t = 0; t < na; ++t) {                                                            \
+        c3d::Mat am = c3d::from_c(cb, a[t]), bm = c3d::from_c(cb, b[t]), cm = mat_dest(c[t]);   \
+        c3d::name(cb, mode, am, bm, cm, as_stream(stream));                                     \
+        c3d::to_c(cm, &c[t]);                                                                   \
+      }                                                                                         \
+    });                                                                                         \
+  }
+#define C3D_BATCHED_BWD(name)                                                                   \
+  int c3d_batched_##name(c3d_cube* cube, int mode, int ndc, const c3d_matrix* dc, int na,       \
+                         const c3d_matrix* a, int nb, const c3d_matrix* b, c3d_matrix* da,      \
+                         c3d_matrix* db, void* stream) {                                        \
+    return guard([&] {                                                                          \
+      require_same_batch(na, nb);                                                               \
+      require_same_batch(na, ndc);                                                              \
+      auto& cb = get(cube);                                                                     \
+      for (int t = 0; t < na; ++t) {                                                            \
+        c3d::Mat dcm = c3d::from_c(cb, dc[t]), am = c3d::from_c(cb, a[t]),                      \
+                 bm = c3d::from_c(cb, b[t]);                                                    \
+        c3d::Mat dam = mat_dest(da[t]), dbm = mat_dest(db[t]);                                  \
+        c3d::name(cb, mode, dcm, am, bm, dam, dbm, as_stream(stream));                          \
+        c3d::to_c(dam, &da[t]);                                                                 \
+        c3d::to_c(dbm, &db[t]);                                                                 \
+      }                                                                                         \
+    });                                                                                         \
+  }
+C3D_BATCHED_FWD(matmul_ab_fwd)
+C3D_BATCHED_FWD(matmul_abt_fwd)
+C3D_BATCHED_FWD(matmul_atb_fwd)
+C3D_BATCHED_BWD(matmul_ab_bwd)
+C3D_BATCHED_BWD(matmul_abt_bwd)
+C3D_BATCHED_BWD(matmul_atb_bwd)
+
 // ---------------------------------------------------------------- vector ops
 int c3d_add_vec_fwd(c3d_cube* cube, const c3d_matrix* a, const c3d_vector* b, c3d_matrix* c,
                     void* stream) {

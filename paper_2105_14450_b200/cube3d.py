@@ -423,11 +423,13 @@ class Cube:
              buf.numel(), c3d_dtype(buf), _stream(stream))
         return buf
 
-    def all_gather(self, axis: int, shard, stream=None):
-        """-> (p * numel,) tensor: the members' shards in ascending position order."""
+    def all_gather(self, axis: int, shard, stream=None, out=None):
+        """-> (p * numel,) tensor (or `out`): the members' shards in ascending position
+        order."""
         torch = _torch()
-        out = torch.empty(self.dims[axis] * shard.numel(), dtype=shard.dtype,
-                          device=shard.device)
+        if out is None:
+            out = torch.empty(self.dims[axis] * shard.numel(), dtype=shard.dtype,
+                              device=shard.device)
         call("c3d_all_gather", self._h, axis, C.c_void_p(shard.data_ptr()),
              C.c_void_p(out.data_ptr()), shard.numel(), c3d_dtype(shard), _stream(stream))
         return out
@@ -554,6 +556,46 @@ def matmul_abt_bwd(cube, dc, a, b, mode=MODE_AUTO, out_dtype=None, stream=None):
 def matmul_atb_bwd(cube, dc, a, b, mode=MODE_AUTO, out_dtype=None, stream=None):
     """cube3d/ops3d.hpp:252-277."""
     return _bwd("c3d_matmul_atb_bwd", cube, dc, a, b, mode, out_dtype, stream)
+
+
+# ------------------------------------------------------------ batched matmuls
+# cube3d/ops3d.hpp:418-494 (BatchedShardedMatrix = a list of ShardedMatrix slices)
+
+_FWD_SHAPE = {"ab": lambda a, b: (a.global_rows, b.global_cols, OUTPUT, a.dirs.swapped()),
+              "abt": lambda a, b: (a.global_rows, b.global_rows, OUTPUT, a.dirs.swapped()),
+              "atb": lambda a, b: (a.global_cols, b.global_cols, WEIGHT, a.dirs)}
+
+
+def _arr(ms):
+    return (L.c3d_matrix * max(1, len(ms)))(*[m.c() for m in ms])
+
+
+def batched_matmul_fwd(form: str, cube: Cube, a: Sequence[ShardedMatrix],
+                       b: Sequence[ShardedMatrix], mode=MODE_AUTO, out_dtype=None, stream=None):
+    """batched_matmul_{ab,abt,atb}_fwd: one 3-D product per slice; BatchMismatch when the
+    slice counts differ."""
+    outs = []
+    for x, y in zip(a, b):
+        r, c, lay, d = _FWD_SHAPE[form](x, y)
+        dt = c3d_dtype(x.shard) if out_dtype is None else out_dtype
+        outs.append(_out_matrix(cube, r, c, lay, d, dt))
+    ca, cb, cc = _arr(a), _arr(b), _arr(outs)
+    call(f"c3d_batched_matmul_{form}_fwd", cube.handle, mode, len(a), ca, len(b), cb, cc,
+         _stream(stream))
+    return outs
+
+
+def batched_matmul_bwd(form: str, cube: Cube, dc, a, b, mode=MODE_AUTO, out_dtype=None,
+                       stream=None):
+    """batched_matmul_{ab,abt,atb}_bwd -> (list of dA, list of dB)."""
+    das, dbs = [], []
+    for g, x, y in zip(dc, a, b):
+        dt = c3d_dtype(g.shard) if out_dtype is None else out_dtype
+        das.append(_out_matrix(cube, x.global_rows, x.global_cols, x.layout, x.dirs, dt))
+        dbs.append(_out_matrix(cube, y.global_rows, y.global_cols, y.layout, y.dirs, dt))
+    call(f"c3d_batched_matmul_{form}_bwd", cube.handle, mode, len(dc), _arr(dc), len(a), _arr(a),
+         len(b), _arr(b), _arr(das), _arr(dbs), _stream(stream))
+    return das, dbs
 
 
 # ------------------------------------------------------------ vector ops

@@ -123,3 +123,41 @@ def test_vector_ops(cube, mul):
     assert O.rel_err(to_np(Cm.shard), want_c) < 1e-6
     assert O.rel_err(to_np(dA.shard), want_da) < 1e-6
     assert O.rel_err(to_np(db.shard), want_db) < 1e-5
+
+
+@pytest.mark.parametrize("form", ["ab", "abt", "atb"])
+def test_batched_matmuls_equal_the_loop(cube, form):
+    """batched_matmul_*_fwd/bwd (cube3d/ops3d.hpp:418-494): each slice equals its
+    unbatched product bitwise and the counters equal the looped accounting
+    (tests/test_ops3d.cpp:506-537); differing extents raise BatchMismatch."""
+    import torch
+    F = {"ab": "AB", "abt": "ABt", "atb": "AtB"}[form]
+    la, lb, lg, bdirs = FORM_LAYOUTS[F]
+    r = O.Rng(13)
+    M, N, K = 128, 64, 192
+    slices = []
+    for _ in range(3):
+        a = O.random_integer_matrix(M, N, r)
+        b = O.random_integer_matrix(*((N, K) if F == "AB" else (K, N) if F == "ABt" else (M, K)), r)
+        g = O.random_integer_matrix(*((M, K) if F != "AtB" else (N, K)), r)
+        slices.append((c3.shard_to_device(cube, a, la, c3.BF16),
+                       c3.shard_to_device(cube, b, lb, c3.BF16, bdirs),
+                       c3.shard_to_device(cube, g, lg, c3.BF16)))
+    A, B, G = ([s[k] for s in slices] for k in range(3))
+    cube.reset_counters()
+    cs = c3.batched_matmul_fwd(form, cube, A, B, c3.MODE_TC, c3.F32)
+    das, dbs = c3.batched_matmul_bwd(form, cube, G, A, B, c3.MODE_TC, c3.F32)
+    torch.cuda.synchronize()
+    batched = cube.counters()
+    cube.reset_counters()
+    for t in range(3):
+        c = FWD[F](cube, A[t], B[t], c3.MODE_TC, c3.F32)
+        da, db = BWD[F](cube, G[t], A[t], B[t], c3.MODE_TC, c3.F32)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(cs[t].shard), to_np(c.shard))
+        assert np.array_equal(to_np(das[t].shard), to_np(da.shard))
+        assert np.array_equal(to_np(dbs[t].shard), to_np(db.shard))
+    assert cube.counters() == batched
+    with pytest.raises(C3DError) as e:
+        c3.batched_matmul_fwd(form, cube, A, B[:2], c3.MODE_TC, c3.F32)
+    assert e.value.name == "BatchMismatch"

@@ -1,7 +1,7 @@
 """BASELINE.json's other configurations on the current grid (run under torchrun for
 N > 1): cfg1 (3-D C = A B, M=N=K=1024, fp32-exact mode and bf16), cfg2 (3-D Linear fwd+bwd,
 batch*seq = 4096 (b=8, s=512), hidden 2048 -> 8192, bf16), cfg5 (3-D matmul sweep
-M=N=K = 4096..32768, bf16). Device-resident operands, CUDA graphs, CUDA events, max over
+M=N=K = 4096..32768, bf16, next to the 1-D row-partition baseline). Device-resident operands, CUDA graphs, CUDA events, max over
 ranks; whole-job TFLOP/s. Prints one JSON line per measurement on rank 0.
 
 usage: python tools/configs_bench.py [--sizes 4096,8192,16384,32768] [--iters 10]
@@ -83,19 +83,37 @@ def main():
     flops = 3 * 2.0 * bsz * seq * hin * hout
     out({"config": "cfg2 linear3d fwd+bwd b*s=4096 2048->8192", "dtype": "bf16", "ms": ms,
          "tflops": flops / (ms * 1e-3) / 1e12})
-    # cfg5: matmul sweep
+    # cfg5: matmul sweep, 3-D and the 1-D row-partition baseline (baselines.py) on a
+    # (N, 1, 1) line of the same GPUs
+    from paper_2105_14450_b200.baselines import OneDMatmul
+    line = cube if cube.dims == (world, 1, 1) else dist.make_cube((world, 1, 1))
+    # each size's 3-D and 1-D runs back to back (the same power / clock state)
     for n in (int(v) for v in args.sizes.split(",")):
+        iters = max(2, args.iters // (n // 4096))
         try:
             a, b = mat(n, n, c3.INPUT, torch.bfloat16), mat(n, n, c3.WEIGHT, torch.bfloat16)
-            ms = timed(lambda: c3.matmul_ab_fwd(cube, a, b), max(2, args.iters // (n // 4096)))
+            ms = timed(lambda: c3.matmul_ab_fwd(cube, a, b), iters)
             out({"config": f"cfg5 matmul_ab_fwd M=N=K={n}", "dtype": "bf16", "ms": ms,
                  "tflops": 2.0 * n ** 3 / (ms * 1e-3) / 1e12})
             del a, b
             torch.cuda.empty_cache()
         except Exception as ex:
             out({"config": f"cfg5 matmul_ab_fwd M=N=K={n}", "error": str(ex)[:200]})
+        try:
+            od = OneDMatmul(line, n)
+            ms = timed(od.step, iters)
+            out({"config": f"cfg5 1-D row-partition matmul M=N=K={n}", "dtype": "bf16", "ms": ms,
+                 "tflops": od.flops() / (ms * 1e-3) / 1e12, "grid_1d": f"{world}x1x1"})
+            del od
+            torch.cuda.empty_cache()
+        except Exception as ex:
+            out({"config": f"cfg5 1-D row-partition matmul M=N=K={n}", "error": str(ex)[:200]})
+    torch.cuda.synchronize()
+    dist.barrier()
+    if line is not cube:
+        line.close()
     cube.close()
-    os._exit(0)
+    dist.destroy()
 
 
 if __name__ == "__main__":
