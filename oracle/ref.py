@@ -165,3 +165,39 @@ def time_layer(p, b, s, n, h, params, x, dy):
     _chk(lib().ref_time_layer(p, C.c_int64(b), C.c_int64(s), C.c_int64(n), C.c_int64(h),
                               _pp(ps), _dp(x), _dp(dy), secs))
     return secs[0], secs[1]
+
+
+def write_matrix(path, m, f32=False):
+    """The reference's write_matrix_file (cube3d/matrix_io.hpp:83-108)."""
+    m = np.ascontiguousarray(np.atleast_2d(m), dtype=np.float64)
+    _chk(lib().ref_write_matrix(str(path).encode(), C.c_int64(m.shape[0]), C.c_int64(m.shape[1]),
+                                _dp(m), int(f32)))
+
+
+def read_matrix(path, f32=False, cap=1 << 24):
+    rows, cols = C.c_int64(), C.c_int64()
+    buf = np.zeros(cap)
+    _chk(lib().ref_read_matrix(str(path).encode(), int(f32), C.byref(rows), C.byref(cols), _dp(buf),
+                               C.c_int64(cap)))
+    return buf[:rows.value * cols.value].reshape(rows.value, cols.value)
+
+
+def save_layer_params(params, h, prefix):
+    ps = [np.ascontiguousarray(params[f], dtype=np.float64) for f in FIELDS]
+    _chk(lib().ref_save_layer_params(C.c_int64(h), _pp(ps), str(prefix).encode()))
+
+
+def load_layer_params(h, prefix):
+    arrs = [np.zeros(s) for s in param_shapes(h)]
+    _chk(lib().ref_load_layer_params(C.c_int64(h), str(prefix).encode(), _pp(arrs)))
+    return dict(zip(FIELDS, arrs))
+
+
+def scaling_csv(weak, b, s, n, h, layers, p_list, lam=1.0):
+    """cube3d/bench.hpp run_scaling + write_scaling_csv (the CLI's bench subcommand)."""
+    ps = (C.c_int * len(p_list))(*p_list)
+    buf = C.create_string_buffer(1 << 16)
+    _chk(lib().ref_scaling_csv(int(weak), C.c_int64(b), C.c_int64(s), C.c_int64(n), C.c_int64(h),
+                               C.c_int64(layers), ps, len(p_list), C.c_double(lam), buf,
+                               C.c_int64(1 << 16)))
+    return buf.value.decode()

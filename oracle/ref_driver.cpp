@@ -14,6 +14,9 @@
 #include <vector>
 
 #include "cube3d/cost_model.hpp"
+#include "cube3d/matrix_io.hpp"
+#include "cube3d/bench.hpp"
+#include "cube3d/transformer.hpp"
 #include "cube3d/reference.hpp"
 #include "cube3d/rng.hpp"
 #include "cube3d/verify.hpp"
@@ -294,6 +297,53 @@ int ref_time_layer(int p, int64_t b, int64_t s, int64_t n, int64_t h,
     });
     seconds[0] = tf;
     seconds[1] = tb;
+  });
+}
+
+// The reference's own matrix files (cube3d/matrix_io.hpp) and checkpoints
+// (transformer.hpp:259-293), to pin the format of paper_2105_14450_b200/matrix_io.py.
+int ref_write_matrix(const char* path, int64_t rows, int64_t cols, const double* data, int f32) {
+  return guard([&] {
+    if (f32) write_matrix_file(path, to_mat<float>(data, rows, cols));
+    else write_matrix_file(path, to_mat<double>(data, rows, cols));
+  });
+}
+int ref_read_matrix(const char* path, int f32, int64_t* rows, int64_t* cols, double* data,
+                    int64_t cap) {
+  return guard([&] {
+    auto rd = [&](auto m) {
+      *rows = static_cast<int64_t>(m.rows);
+      *cols = static_cast<int64_t>(m.cols);
+      if (data && static_cast<int64_t>(m.data.size()) <= cap) put(m, data);
+    };
+    if (f32) rd(read_matrix_file<float>(path));
+    else rd(read_matrix_file<double>(path));
+  });
+}
+int ref_save_layer_params(int64_t h, const double* const* params, const char* prefix) {
+  return guard([&] {
+    TransformerConfig cfg = make_cfg(1, 1, 1, 1, h);
+    save_layer_params(params_of<double>(cfg, params), prefix);
+  });
+}
+int ref_load_layer_params(int64_t h, const char* prefix, double* const* out) {
+  return guard([&] {
+    (void)h;
+    put_params(load_layer_params<double>(prefix), out);
+  });
+}
+// The bench subcommand's modeled scaling table (cube3d/bench.hpp), as CSV text.
+int ref_scaling_csv(int weak, int64_t b, int64_t s, int64_t n, int64_t h, int64_t layers,
+                    const int* p_list, int np, double lambda, char* buf, int64_t buflen) {
+  return guard([&] {
+    TransformerConfig base = make_cfg(1, b, s, n, h);
+    base.layers = layers;
+    std::vector<int> ps(p_list, p_list + np);
+    auto rows = run_scaling(weak ? ScalingMode::weak : ScalingMode::strong, base, ps, lambda);
+    std::ostringstream os;
+    write_scaling_csv(os, rows);
+    std::strncpy(buf, os.str().c_str(), static_cast<std::size_t>(buflen - 1));
+    buf[buflen - 1] = 0;
   });
 }
 

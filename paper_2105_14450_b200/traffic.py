@@ -121,3 +121,49 @@ def reference_deviation(b: int, s: int, n: int, h: int, p: int,
         "reuse_output_grad_gather": sum((p - 1) * rows * wo for _, wo in lins),
         "rowdot_gather": p ** 3 * slices_per_rank * (p - 1) * (s - s // p) if flash else 0,
     }
+
+
+def layer_madds(b: int, s: int, n: int, h: int, p: int) -> Tuple[int, int]:
+    """Per-rank multiply-adds of one layer (fwd, bwd) on a p-cube: madds::transformer_layer_*
+    (cube3d/cost_model.hpp:172-208); the library charges the same counts."""
+    rows = b * s
+    mm = lambda m, k, nn: (m // p) * (k // p) * (nn // p)  # noqa: E731
+    slices = (b // p) * (n // p)
+    core = slices * 2 * s * (s // p) * (h // n)
+    fwd = mm(rows, h, 3 * h) + core + mm(rows, h, h) + mm(rows, h, 4 * h) + mm(rows, 4 * h, h)
+    return fwd, 2 * fwd
+
+
+def scaling_rows(mode: str, b: int, s: int, n: int, h: int, layers: int, p_list: Sequence[int],
+                 lam: float = 1.0, reference_traffic: bool = False):
+    """The CLI bench table (cube3d/bench.hpp:41-93): modeled cost units per rank per step
+    (multiply-adds + lam x communicated elements) for each cube side; weak scaling grows
+    batch x p, hidden x p^2, heads x p. `reference_traffic`: charge the reference's traffic
+    model (this library's plus the documented reuse terms) instead of this library's."""
+    rows = []
+    for p in p_list:
+        if p < 1:
+            raise ValueError("cube side must be positive")
+        bb, hh, nn = (b * p, h * p * p, n * p) if mode == "weak" else (b, h, n)
+        # TransformerConfig::validate (cube3d/nn.hpp:29-40)
+        if bb % p or s % p or hh % (p * p) or (4 * hh) % (p * p) or nn % p or hh % nn:
+            raise ValueError(f"configuration (b={bb}, s={s}, heads={nn}, h={hh}) is not "
+                             f"divisible on the p={p} cube")
+        f, bw = layer_traffic(bb, s, nn, hh, (p, p, p),
+                              flash=flash_applies(s, nn, hh, (p, p, p), True))
+        if reference_traffic and p > 1:
+            bw += sum(reference_deviation(bb, s, nn, hh, p, flash_applies(s, nn, hh, (p, p, p),
+                                                                          True)).values())
+        p3 = p ** 3
+        mf, mb = layer_madds(bb, s, nn, hh, p)
+        fc = layers * (mf + lam * (f // p3))
+        bc = layers * (mb + lam * (bw // p3))
+        rows.append((p3, bb, hh, float(fc), float(bc), (fc + bc) / bb))
+    return rows
+
+
+def scaling_csv(rows) -> str:
+    out = ["gpus,batch,hidden,forward_cost,backward_cost,avg_step_cost"]
+    for g, b, h, f, bw, a in rows:
+        out.append(f"{g},{b},{h},{f:.6f},{bw:.6f},{a:.6f}")
+    return "\n".join(out) + "\n"
