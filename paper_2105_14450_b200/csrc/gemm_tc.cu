@@ -67,8 +67,8 @@ struct TcArgs {
   int cw;                    // columns per store chunk (32 fp32, 64 bf16)
   int st_rsplit, st_csplit;  // split of the stored view (rows / cols)
   int st_blo;                // batch-lo extent of the stored view
-  int x_tma;                 // 1: aux tile chunks arrive by TMA (tmP) into a second
-                             //    per-warp buffer (same view geometry as the output)
+  int x_tma;                 // 1: aux (2: residual) tile chunks arrive by TMA (tmP) into
+                             //    a second per-warp buffer (same view geometry as the output)
   int pre_tma;               // 1: the pre-activation output is staged in that second
                              //    buffer and TMA-stored through tmP
   TcOperand a, b;
@@ -402,7 +402,10 @@ __device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, in
     }
   }
   if (e.resid != nullptr && row_ok) {
-    if (vec) {
+    if (args.x_tma == 2) {  // the residual chunk arrived by TMA into xbuf
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] += smem_at<CW>(xbuf, lane, 32 * h + j);
+    } else if (vec) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8) {
         float r[8];
@@ -953,13 +956,16 @@ bool operand_ok(const View& v, long long rows, long long cols, int tile_rows) {
 // when fewer than half the SMs would get a tile, maximising wave efficiency
 // (units / (waves * SMs)) with >= 16 K-blocks per split (measured on B200: splitting
 // a 128-tile GEMM loses to the extra partial-sum traffic; a 32-tile one gains 2x).
-int pick_ksplit(long long M, long long N, int tiles, int k_blocks, int batch, int num_sms) {
+int pick_ksplit(long long M, long long N, int tiles, int k_blocks, int batch, int num_sms, int bn) {
   (void)M;
   (void)N;
+  (void)bn;
   if (const char* env = std::getenv("C3D_KSPLIT")) {  // experiments only
     const int ks = std::atoi(env);
     if (ks >= 1 && batch == 1) return std::min(ks, std::max(1, k_blocks / 4));
   }
+  // measured: with >= num_sms / 2 tiles the partial-sum traffic costs more than the
+  // idle SMs (e.g. 96 tiles of 1024 x 3072 x 16384: 112 us unsplit, 118 us at 3 splits)
   if (batch != 1 || 2 * tiles > num_sms) return 1;
   int best = 1;
   double best_eff = static_cast<double>(tiles) / num_sms;
@@ -1056,7 +1062,8 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.group_m = (p.N * p.K * 2 > (48ll << 20)) ? std::min(16, args.m_tiles) : 1;
   if (const char* e = std::getenv("C3D_GROUP_M")) args.group_m = std::max(1, std::min(std::atoi(e), args.m_tiles));
   args.ksplit = p.rs.P > 1 ? 1
-                            : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms);
+                            : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms,
+                                          bn);
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
   args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
   args.epi = p.epi;
@@ -1110,6 +1117,11 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     } else if (p.epi.aux && p.epi.aux_dtype == p.epi.out.dtype) {
       xv.base = const_cast<void*>(p.epi.aux);
       if (make_store_map(xv, p.M, p.N, p.batch, args.cw, &mp)) args.x_tma = 1;
+    } else if (p.epi.resid && !p.epi.aux && p.epi.resid_dtype == p.epi.out.dtype &&
+               args.k_blocks <= 16) {
+      // short K: the residual read dominates the epilogue, worth a pipeline stage of smem
+      xv.base = const_cast<void*>(p.epi.resid);
+      if (make_store_map(xv, p.M, p.N, p.batch, args.cw, &mp)) args.x_tma = 2;
     }
   }
   RsMaps rsm;
