@@ -55,6 +55,7 @@ struct TcOperand {
 
 struct TcArgs {
   int M, N, K, batch;
+  int cg;  // CTAs per tile (2: cta_group::2 pair, M = 256)
   int m_tiles, n_tiles, k_blocks;
   int group_m;  // tile rows per rasterisation band (1: plain m-major order)
   int num_tiles;  // output tiles (batch * m_tiles * n_tiles)
@@ -164,11 +165,28 @@ __device__ __forceinline__ void op_issue(const CUtensorMap* map, const TcOperand
   }
 }
 
+// Same for a CTA pair: the load lands in this CTA's shared memory and completes on the
+// leader's full barrier (shared::cluster address `bar`).
+template <int ROWS>
+__device__ __forceinline__ void op_issue_pair(const CUtensorMap* map, const TcOperand& op,
+                                              const OpPos& p, uint8_t* dst, uint32_t bar) {
+  if (!op.mn_major) {
+    ptx::tma_load_5d_pair(dst, map, bar, p.k_lo, p.r_lo[0], p.r_hi[0] + p.k_hi, p.c3, p.c4);
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS / 64; ++j)
+      ptx::tma_load_5d_pair(dst + j * 8192, map, bar, p.r_lo[j], p.k_lo, p.r_hi[j] + p.k_hi, p.c3,
+                            p.c4);
+  }
+}
+
 struct Unit {
   int b, m0, n0, kb0, kb1, ks;
 };
 
-__device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
+// CTA pairs (cg = 2): m tiles are 256-row pair tiles; CTA `rank` owns rows
+// [m0 + 128 rank, +128) of its pair's tile.
+__device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn, int rank = 0) {
   Unit u;
   // split-major order: the persistent CTAs sweep K window by window together, so each
   // window's operand footprint stays resident in L2 (no drift-induced thrash).
@@ -186,7 +204,7 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn) {
   const int within = rem - group * (a.group_m * a.n_tiles);
   const int nt = within / gsize;
   const int mt = first_m + (within - nt * gsize);
-  u.m0 = mt * kBM;
+  u.m0 = mt * kBM * a.cg + rank * kBM;
   u.n0 = nt * bn;
   u.kb0 = u.ks * a.kb_per_split;
   u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
@@ -324,11 +342,11 @@ __device__ __forceinline__ float smem_at(const uint8_t* xbuf, int lane, int j) {
 template <int CW>
 __device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, int n0, float (&v)[32],
                                            bool row_ok, bool vec, uint8_t* xbuf, int lane,
-                                           int h, float rv) {
+                                           int h, float rv, bool applied = false) {
   const Epilogue& e = args.epi;
   const int nvalid = min(32, args.N - n0);
-  // the pre-activation pass already wrote gelu(alpha * acc + bias) back to TMEM
-  const bool applied = args.pre_tma && e.pre_act != nullptr && e.act == kActGeluSave;
+  // applied: v already holds alpha * acc + bias (and gelu of it for kActGeluSave), the
+  // pre-activation value having been staged by epi_tile_tma
   if (e.alpha != 1.f && !applied) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
@@ -347,7 +365,7 @@ __device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, in
     }
   }
   if (e.pre_act != nullptr && args.pre_tma) {
-    // stored by the separate staging pass of epi_tile_tma
+    // staged and stored by epi_tile_tma
   } else if (e.pre_act != nullptr && row_ok) {
     if (e.act == kActGeluSave) {
 #pragma unroll
@@ -457,14 +475,12 @@ __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorM
         row_off + (e.out.csplit ? (n % e.out.csplit) + (n / e.out.csplit) * e.out.s_hi : n);
     const bool vec = live && args.ksplit == 1 && row_ok && args.vec_ok && n + CW <= args.N;
     if (args.pre_tma && live && args.ksplit == 1) {
-      // pre-activation pass: alpha * acc + bias (or gelu'(x) for kActGeluSave) staged and
-      // TMA-stored, then the main pass re-reads TMEM
-      int c0p, c2p;
-      coords(n, c0p, c2p);
+      // one pass: alpha * acc + bias, the pre-activation value (gelu'(x) for kActGeluSave)
+      // staged in xbuf, the output in buf, two TMA stores
       staging_acquire(lane);
 #pragma unroll
       for (int h = 0; h < CW / 32; ++h) {
-        float v[32];
+        float v[32], pre[32];
         ptx::tmem_ld32(row_taddr + cc * CW + 32 * h, v);
         const int nh = n + 32 * h;
         if (e.alpha != 1.f) {
@@ -485,16 +501,27 @@ __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorM
           }
         }
         if (e.act == kActGeluSave) {
-          // gelu goes back to TMEM for the main pass, gelu' to the staging buffer
-          float g[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) gelu_both(v[j], g[j], v[j]);
-          ptx::tmem_st32(row_taddr + cc * CW + 32 * h, g);
+          for (int j = 0; j < 32; ++j) {
+            const float x = v[j];
+            gelu_both(x, v[j], pre[j]);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) pre[j] = v[j];
         }
+#pragma unroll
+        for (int q = 0; q < 32 / VPC; ++q)
+          stage_chunk<CW>(xbuf, lane, h * (32 / VPC) + q, pre + VPC * q);
+        epi_math32<CW>(args, off + 32 * h, nh, v, row_ok, vec, xbuf, lane, h, rv, true);
 #pragma unroll
         for (int q = 0; q < 32 / VPC; ++q) stage_chunk<CW>(buf, lane, h * (32 / VPC) + q, v + VPC * q);
       }
-      store_staged(tmX, buf, lane, c0p, c1, c2p, c3, c4);
+      int c0, c2;
+      coords(n, c0, c2);
+      store_staged(tmX, xbuf, lane, c0, c1, c2, c3, c4);
+      store_staged(tmC, buf, lane, c0, c1, c2, c3, c4);
+      continue;
     }
     staging_acquire(lane);
     if (args.x_tma && live) {
@@ -526,7 +553,11 @@ __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorM
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with tcgen05.mma.cta_group::2:
+// each CTA stages its 128 rows of A and its BN/2 rows of B (half the operand bytes per SM),
+// the leader's single thread issues the M = 256 MMAs and commits to both CTAs' barriers,
+// and each CTA's epilogue drains its own 128 TMEM lanes.
+template <int BN, bool A_MN, bool B_MN, int CG = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB,
@@ -534,10 +565,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmP, const TcArgs args,
                    const __grid_constant__ RsMaps rsm) {
   constexpr int kABytes = kBM * kBK * 2;  // 16 KB
-  constexpr int kBBytes = BN * kBK * 2;
+  constexpr int kBRows = BN / CG;         // B rows staged by this CTA
+  constexpr int kBBytes = kBRows * kBK * 2;
   constexpr int kStageBytes = kABytes + kBBytes;
   constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+  constexpr uint32_t kIdesc = ptx::idesc_bf16_f32(kBM * CG, BN, A_MN, B_MN);
+  const int rank = CG == 2 ? static_cast<int>(ptx::cluster_rank()) : 0;
+  const int cta_id = blockIdx.x / CG, cta_stride = gridDim.x / CG;
   constexpr int kColsPerWarp = BN / 2;  // two epilogue warps per lane quarter
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -548,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem_b = smem + S * kABytes;
   uint8_t* smem_stage = smem + S * kStageBytes;  // 8 epilogue warps x 4 KB, 1024-aligned
   uint8_t* smem_x = smem_stage + kEpiWarps * 4096;  // operand chunks (x_tma)
-  const int staging = args.tma_store ? kEpiWarps * 4096 * (args.x_tma ? 2 : 1) : 0;
+  const int staging = args.tma_store ? kEpiWarps * 4096 * ((args.x_tma || args.pre_tma) ? 2 : 1) : 0;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStageBytes + staging);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
@@ -569,14 +603,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull_bar[s], 1);
-      ptx::mbar_init(&tempty_bar[s], kEpiWarps);
+      ptx::mbar_init(&tempty_bar[s], kEpiWarps * CG);  // both CTAs' epilogues (leader's)
     }
     for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(&x_bar[w], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (CG == 2) ptx::tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // the peer's barriers exist before any remote arrive
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -586,15 +624,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       OpPos pa, pb;
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
-        const Unit u = decode_unit(args, t, BN);
+      const uint32_t full_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(full_bar), 0) : 0u;
+      for (int t = cta_id; t < units; t += cta_stride) {
+        const Unit u = decode_unit(args, t, BN, rank);
         op_init(args.a, pa, u.m0, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
-        op_init(args.b, pb, u.n0, B_MN ? BN / 64 : 1, u.kb0 * kBK, u.b);
+        op_init(args.b, pb, u.n0 + rank * kBRows, B_MN ? kBRows / 64 : 1, u.kb0 * kBK, u.b);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
           ptx::mbar_wait(&empty_bar[s], ph ^ 1);
-          ptx::mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
-          op_issue<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
-          op_issue<BN>(&tmB, args.b, pb, smem_b + s * kBBytes, &full_bar[s]);
+          if (CG == 2) {
+            // the leader expects both CTAs' bytes; the peer's loads only complete_tx on the
+            // leader's barrier (a remote release-arrive would cost a membar per stage)
+            const uint32_t fb = full_leader + s * 8;
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * kStageBytes);
+            op_issue_pair<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, fb);
+            op_issue_pair<kBRows>(&tmB, args.b, pb, smem_b + s * kBBytes, fb);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full_bar[s], kStageBytes);
+            op_issue<kBM>(&tmA, args.a, pa, smem_a + s * kABytes, &full_bar[s]);
+            op_issue<BN>(&tmB, args.b, pb, smem_b + s * kBBytes, &full_bar[s]);
+          }
           op_advance(args.a, pa);
           op_advance(args.b, pb);
           if (++s == S) {
@@ -605,14 +653,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- UMMA issuer
+    if (lane == 0 && rank == 0) {
+      // ---------------- UMMA issuer (the pair's leader for CG = 2)
       int s = 0;
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
       const uint32_t a0 = ptx::smem_u32(smem_a), b0 = ptx::smem_u32(smem_b);
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+      for (int t = cta_id; t < units; t += cta_stride) {
         const Unit u = decode_unit(args, t, BN);
         ptx::mbar_wait(&tempty_bar[acc], aph ^ 1);
         ptx::tc_fence_after();
@@ -628,15 +676,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : ptx::smem_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? ptx::smem_desc_sw128(b_addr + k * 2048, 8192, 1024)
                                      : ptx::smem_desc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::umma_bf16(tmem_d, ad, bd, kIdesc, (kb > u.kb0 || k > 0) ? 1u : 0u);
+            if (CG == 2) ptx::umma_bf16_pair(tmem_d, ad, bd, kIdesc, (kb > u.kb0 || k > 0) ? 1u : 0u);
+            else ptx::umma_bf16(tmem_d, ad, bd, kIdesc, (kb > u.kb0 || k > 0) ? 1u : 0u);
           }
-          ptx::umma_commit(&empty_bar[s]);
+          if (CG == 2) ptx::umma_commit_pair(&empty_bar[s], 3);
+          else ptx::umma_commit(&empty_bar[s]);
           if (++s == S) {
             s = 0;
             ph ^= 1;
           }
         }
-        ptx::umma_commit(&tfull_bar[acc]);
+        if (CG == 2) ptx::umma_commit_pair(&tfull_bar[acc], 3);
+        else ptx::umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -660,8 +711,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  e.pre_act != nullptr);
       const uint32_t epoch = args.rs_P ? *args.rs_epoch : 0u;
       uint32_t entered_mask = 0;
-      for (int t = blockIdx.x; t < units; t += gridDim.x) {
-        const Unit u = decode_unit(args, t, BN);
+      for (int t = cta_id; t < units; t += cta_stride) {
+        const Unit u = decode_unit(args, t, BN, rank);
         const int mrow0 = u.m0 + quarter * 32;
         const int m = mrow0 + lane;
         const bool row_ok = m < args.M;
@@ -697,7 +748,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               c2r, c3, c4);
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+        if (lane == 0) {
+          if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty_bar[acc]), 0));
+          else ptx::mbar_arrive(&tempty_bar[acc]);
+        }
         if (++acc == 2) {
           acc = 0;
           aph ^= 1;
@@ -713,8 +767,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else
-    for (int t = blockIdx.x; t < units; t += gridDim.x) {
-      const Unit u = decode_unit(args, t, BN);
+    for (int t = cta_id; t < units; t += cta_stride) {
+      const Unit u = decode_unit(args, t, BN, rank);
       const int m = u.m0 + quarter * 32 + lane;
       // row offset once per unit (the only divisions on the epilogue path)
       long long row_off = 0;
@@ -750,7 +804,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if (CG == 2) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty_bar[acc]), 0));
+        else ptx::mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         aph ^= 1;
@@ -758,10 +815,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  __syncthreads();
+  ptx::tc_fence_before();
+  if (CG == 2) ptx::cluster_sync();  // no remote arrive or multicast commit still in flight
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<kTmemCols>(tmem_base);
+    if (CG == 2) ptx::tmem_dealloc_pair<kTmemCols>(tmem_base);
+    else ptx::tmem_dealloc<kTmemCols>(tmem_base);
   }
   if (args.rs_P && threadIdx.x == 0) {
     const uint32_t epoch = *args.rs_epoch;
@@ -902,24 +962,56 @@ bool make_store_map(const View& v, long long rows, long long cols, int batch, in
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG = 1>
 void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
                cudaStream_t stream) {
-  constexpr int kStageBytes = (kBM + BN) * kBK * 2;
-  const int staging = args.tma_store ? kEpiWarps * 4096 * (args.x_tma ? 2 : 1) : 0;
+  constexpr int kStageBytes = (kBM + BN / CG) * kBK * 2;
+  const int staging = args.tma_store ? kEpiWarps * 4096 * ((args.x_tma || args.pre_tma) ? 2 : 1) : 0;
   int stages = (kSmemBudget - 1024 - 256 - staging) / kStageBytes;
   stages = std::min(stages, 8);
   args.stages = stages;
   const int smem = 1024 + stages * kStageBytes + staging + (2 * stages + 4 + kEpiWarps) * 8 + 16;
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, CG>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget);
+    if (CG == 2) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     attr_set = true;
   }
-  const int grid = std::min(args.num_tiles * args.ksplit, num_sms);
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mp, args, rsm);
+  const int units = args.num_tiles * args.ksplit;
+  if (CG == 1) {
+    const int grid = std::min(units, num_sms);
+    kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mp, args, rsm);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // A persistent grid must be co-resident: the GPCs' SM counts need not be even, so the
+  // number of resident pairs can be below num_sms / 2 (a second wave would double the time).
+  static int max_pairs = 0;  // per instantiation (smem is fixed per instantiation)
+  if (max_pairs == 0) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      (void)cudaGetLastError();
+      n = num_sms / 2;
+    }
+    max_pairs = std::min(n, num_sms / 2);
+    if (std::getenv("C3D_GEMM_VERBOSE"))
+      std::fprintf(stderr, "tc_gemm pair kernel: %d resident pairs\n", max_pairs);
+  }
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_pairs)));
+  C3D_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mp, args, rsm));
 }
 
 template <int BN>
@@ -927,6 +1019,13 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
                const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
                cudaStream_t stream) {
   const bool am = args.a.mn_major, bm = args.b.mn_major;
+  if (BN == 256 && args.cg == 2) {
+    if (!am && !bm) launch_tc<BN, false, false, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+    else if (!am && bm) launch_tc<BN, false, true, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+    else if (am && !bm) launch_tc<BN, true, false, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+    else launch_tc<BN, true, true, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
+    return;
+  }
   if (!am && !bm) launch_tc<BN, false, false>(ma, mb, mc, mp, args, rsm, num_sms, stream);
   else if (!am && bm) launch_tc<BN, false, true>(ma, mb, mc, mp, args, rsm, num_sms, stream);
   else if (am && !bm) launch_tc<BN, true, false>(ma, mb, mc, mp, args, rsm, num_sms, stream);
@@ -1054,6 +1153,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.N = static_cast<int>(p.N);
   args.K = static_cast<int>(p.K);
   args.batch = p.batch;
+  args.cg = 1;
   args.m_tiles = static_cast<int>((p.M + kBM - 1) / kBM);
   args.n_tiles = static_cast<int>((p.N + bn - 1) / bn);
   args.k_blocks = static_cast<int>((p.K + kBK - 1) / kBK);
@@ -1066,6 +1166,14 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
                                           bn);
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
   args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
+  // CTA pairs (cta_group::2, 256 x 256 tiles) for plain 256-wide tiles
+  if (bn == 256 && args.ksplit == 1 && p.rs.P <= 1 && !std::getenv("C3D_NO_CG2") &&
+      args.m_tiles >= 2) {
+    args.cg = 2;
+    args.m_tiles = static_cast<int>((p.M + 2 * kBM - 1) / (2 * kBM));
+    args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
+    args.group_m = std::min(args.group_m, args.m_tiles);
+  }
   args.epi = p.epi;
   // vector loads/stores need 16-B aligned rows and 32-column chunks
   const int esz = p.epi.out.dtype == kF32 ? 4 : 2;
@@ -1082,7 +1190,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   if (args.ksplit > 1) vec = vec && (p.N % 4 == 0);
   args.vec_ok = vec ? 1 : 0;
   CUtensorMap ma = make_operand_map(p.a, p.M, p.K, p.batch, kBM, &args.a);
-  CUtensorMap mb = make_operand_map(p.b, p.N, p.K, p.batch, bn, &args.b);
+  CUtensorMap mb = make_operand_map(p.b, p.N, p.K, p.batch, bn / args.cg, &args.b);
   float* ws = nullptr;
   if (args.ksplit > 1) {
     C3D_CUDA(cudaMallocAsync(&ws, sizeof(float) * args.ksplit * p.M * p.N, stream));
