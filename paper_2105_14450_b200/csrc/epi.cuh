@@ -11,10 +11,12 @@ namespace c3d {
 // Abramowitz & Stegun 7.1.26 (|error| < 1.5e-7): one reciprocal, one exp and five FMAs,
 // and the exp e^{-z^2} = e^{-x^2/2} is the Gaussian density gelu' needs as well.
 __device__ __forceinline__ void phi_both(float x, float& cdf, float& pdf) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  float t;  // 1 / (1 + p z) by MUFU.RCP (1 ulp; the IEEE-rounded form adds a slow path)
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.f)));
-  const float e = __expf(-z * z);
+  // t = 1 / (1 + p z), z = |x| / sqrt(2); e = e^{-z^2} = 2^{-x^2 log2(e) / 2}. MUFU.RCP and
+  // MUFU.EX2 with flush-to-zero (the IEEE-rounded reciprocal and the denormal-preserving
+  // exp add a slow path / range fix-up per element; e underflows only where erf is 1).
+  float t, e;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.f)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * x * -0.72134752044448170f));
   const float poly =
       t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f),
                       -0.284496736f),

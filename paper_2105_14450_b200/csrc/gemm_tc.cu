@@ -339,6 +339,21 @@ __device__ __forceinline__ float smem_at(const uint8_t* xbuf, int lane, int j) {
 // aux (x_tma 1) or residual (x_tma 2) values, TMA-loaded into shared memory. `rv`: the
 // row's kActSoftmaxBwd value, alpha * rowvec[row]. A pre-activation output is written
 // with direct 16-B stores (the staging buffer carries the main output only).
+// Bias values of columns [n0, n0 + 32) (zero past N).
+__device__ __forceinline__ void load_bias32(const float* bias, int n0, int N, int vec_ok,
+                                            float (&bb)[32]) {
+  if (n0 + 32 <= N && vec_ok) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
+      bb[j] = b4.x; bb[j + 1] = b4.y; bb[j + 2] = b4.z; bb[j + 3] = b4.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bb[j] = n0 + j < N ? bias[n0 + j] : 0.f;
+  }
+}
+
 template <int CW>
 __device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, int n0, float (&v)[32],
                                            bool row_ok, bool vec, uint8_t* xbuf, int lane,
@@ -481,24 +496,17 @@ __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorM
 #pragma unroll
       for (int h = 0; h < CW / 32; ++h) {
         float v[32], pre[32];
-        ptx::tmem_ld32(row_taddr + cc * CW + 32 * h, v);
         const int nh = n + 32 * h;
+        ptx::tmem_ld32(row_taddr + cc * CW + 32 * h, v);
         if (e.alpha != 1.f) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] *= e.alpha;
         }
         if (e.bias != nullptr) {
-          if (nh + 32 <= args.N && args.vec_ok) {
+          float bb[32];
+          load_bias32(e.bias, nh, args.N, args.vec_ok, bb);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 bb = __ldg(reinterpret_cast<const float4*>(e.bias + nh + j));
-              v[j] += bb.x; v[j + 1] += bb.y; v[j + 2] += bb.z; v[j + 3] += bb.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (nh + j < args.N) v[j] += e.bias[nh + j];
-          }
+          for (int j = 0; j < 32; ++j) v[j] += bb[j];
         }
         if (e.act == kActGeluSave) {
 #pragma unroll

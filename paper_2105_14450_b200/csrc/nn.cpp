@@ -574,16 +574,25 @@ void mlp_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const Linear
   void* h1_data = S.keep(DevBuf(hbytes, s)).get();
   h1.dtype = dt;
   S.pre_act = S.keep(DevBuf(hbytes, s)).get();
-  // FC1 writes the pre-activation x into S.pre_act; one elementwise pass then produces
-  // h1 = gelu(x) and leaves gelu'(x) in S.pre_act for the backward (which only
-  // multiplies, kActMulAux) -- cheaper than carrying the erf in the GEMM epilogue
-  Act pre;
-  pre.data = S.pre_act;
-  pre.dtype = dt;
-  linear_fwd(cube, mode, x, fc1, group, pre, &S.fc1_lin, own_input, LinearEpi{}, s, fc1_pre);
-  h1 = pre;
-  h1.data = h1_data;
-  k_gelu_save(S.pre_act, dt, h1.data, dt, static_cast<int64_t>(pre.elems()), s);
+  // h1 = gelu(x), and gelu'(x) kept in S.pre_act for the backward (which only multiplies,
+  // kActMulAux). Without a reduce-scatter after FC1 the GEMM epilogue produces both from
+  // the fp32 accumulator; otherwise FC1 writes x into S.pre_act after the reduction and
+  // one elementwise pass produces both.
+  if (cube.extent(fc1.w.dirs.out) == 1) {
+    h1.data = h1_data;
+    LinearEpi e1;
+    e1.act = kActGeluSave;
+    e1.pre_act = S.pre_act;
+    linear_fwd(cube, mode, x, fc1, group, h1, &S.fc1_lin, own_input, e1, s, fc1_pre);
+  } else {
+    Act pre;
+    pre.data = S.pre_act;
+    pre.dtype = dt;
+    linear_fwd(cube, mode, x, fc1, group, pre, &S.fc1_lin, own_input, LinearEpi{}, s, fc1_pre);
+    h1 = pre;
+    h1.data = h1_data;
+    k_gelu_save(S.pre_act, dt, h1.data, dt, static_cast<int64_t>(pre.elems()), s);
+  }
   LinearEpi e2;
   e2.resid = resid;
   linear_fwd(cube, mode, h1, fc2, group, y, &S.fc2_lin, false, e2, s, fc2_pre);
