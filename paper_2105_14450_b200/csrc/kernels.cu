@@ -125,97 +125,100 @@ __global__ void colsum_partial_kernel(const void* x, int xdt, const void* y, int
   }
   partial[blockIdx.y * cols + c] = acc;
 }
-// Column sums at HBM speed: a CTA of 8 warps covers 256 columns (8 per lane, 16-B loads)
-// x 128 rows (16 per warp, all loads of a warp issued before they are summed), so 4-8
-// resident CTAs keep >= 64 KB per SM in flight. Warps combine through shared memory in a
+// Column sums at HBM speed: a CTA of 32 warps covers 256 columns (8 per lane, 16-B loads)
+// x `rows_per_cta` rows (the launcher sizes the grid to one wave, one CTA per SM; a warp
+// issues 2-8 row loads before summing them), so >= 64 KB per SM stay in flight. Warps combine through shared memory in a
 // fixed order into a per-chunk partial; the last CTA of each column tile (counter) sums
 // the chunks in chunk order -- deterministic, and no second launch. With DUAL, one pass
 // over x yields both colsum(x * y) (out) and colsum(x) (out2): LayerNorm's dgamma and
 // dbeta.
-constexpr int kCsRows = 128, kCsWarpRows = 16;
+constexpr int kCsWarps = 32;
 template <int XDT, int YDT, bool DUAL>
-__global__ void __launch_bounds__(256) colsum_chunk_kernel(const void* x, const void* y, int64_t rows,
-                                                           int64_t cols, float* partial,
-                                                           unsigned* counters, float* out,
-                                                           float* out2) {
+__global__ void __launch_bounds__(32 * kCsWarps, 1) colsum_chunk_kernel(const void* x, const void* y, int64_t rows,
+                                                              int64_t cols, int64_t rows_per_cta,
+                                                              float* partial, unsigned* counters,
+                                                              float* out, float* out2) {
   constexpr int NS = DUAL ? 2 : 1;
-  __shared__ float red[NS][8][256];
+  __shared__ float red[kCsWarps][256];
   __shared__ unsigned last;
   const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
   const int64_t c8 = blockIdx.x * 256LL + lane * 8;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kCsRows + w * kCsWarpRows;
-  auto load8 = [&](const void* base, int dt, int64_t off, float (&v)[8]) {
+  const int64_t rbeg = static_cast<int64_t>(blockIdx.y) * rows_per_cta;
+  const int64_t rend = min(rows, rbeg + rows_per_cta);
+  // raw 16-B words stay in registers until summed (8 values: one word bf16, two fp32)
+  constexpr int QX = XDT == kBF16 ? 1 : 2, QY = YDT == kF32 ? 2 : 1;
+  // 8 values of a raw word group: bf16 -> fp32 is a shift / mask of the 32-bit pair
+  auto val = [](int dt, const uint4* q, int i) -> float {
     if (dt == kBF16) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + off));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h[i]);
-        v[2 * i] = f.x;
-        v[2 * i + 1] = f.y;
-      }
-    } else {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off));
-      const float4 b = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + off + 4));
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+      const uint32_t u = reinterpret_cast<const uint32_t*>(q)[i / 2];
+      return __uint_as_float((i & 1) ? (u & 0xffff0000u) : (u << 16));
     }
+    return reinterpret_cast<const float*>(q)[i];
   };
   float acc[NS][8];
 #pragma unroll
   for (int k = 0; k < NS; ++k)
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[k][i] = 0.f;
-  if (c8 < cols) {
-    constexpr int U = YDT >= 0 ? 4 : 8;  // loads in flight per operand
-#pragma unroll 1
-    for (int k0 = 0; k0 < kCsWarpRows; k0 += U) {
-      float v[U][8];
+  const int64_t r0 = rbeg + w;
+  const int64_t nr = r0 < rend ? (rend - r0 + kCsWarps - 1) / kCsWarps : 0;  // this warp's rows
+  if (c8 < cols && nr > 0) {
+    // row loads in flight per lane: 32 registers of raw words
+    constexpr int U = 8 / (QX + (YDT >= 0 ? QY : 0));
+    const int64_t stride = kCsWarps * cols;  // elements between this warp's rows
+    const char* px = static_cast<const char*>(x) + (r0 * cols + c8) * (XDT == kBF16 ? 2 : 4);
+    const char* py = YDT >= 0 ? static_cast<const char*>(y) + (r0 * cols + c8) * (YDT == kBF16 ? 2 : 4)
+                              : nullptr;
+    const int64_t sx = stride * (XDT == kBF16 ? 2 : 4), sy = stride * (YDT == kBF16 ? 2 : 4);
+    auto step = [&](int n) {  // n <= U rows: loads first, then the sums
+      uint4 qx[U][QX], qy[U][QY];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t r = r0 + k0 + u;
-        if (r < rows) load8(x, XDT, r * cols + c8, v[u]);
-        else
+        if (u < n) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
-      }
-      if (YDT >= 0) {
-        float g[U][8];
+          for (int i = 0; i < QX; ++i) qx[u][i] = __ldg(reinterpret_cast<const uint4*>(px + u * sx) + i);
+          if (YDT >= 0) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t r = r0 + k0 + u;
-          if (r < rows) load8(y, YDT, r * cols + c8, g[u]);
-          else
-#pragma unroll
-            for (int i = 0; i < 8; ++i) g[u][i] = 0.f;
+            for (int i = 0; i < QY; ++i) qy[u][i] = __ldg(reinterpret_cast<const uint4*>(py + u * sy) + i);
+          }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u) {
+        if (u < n) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (DUAL) acc[1][i] += v[u][i];
-            v[u][i] *= g[u][i];
+            const float v = val(XDT, qx[u], i);
+            if (YDT >= 0) {
+              if (DUAL) acc[1][i] += v;
+              acc[0][i] = fmaf(v, val(YDT, qy[u], i), acc[0][i]);
+            } else {
+              acc[0][i] += v;
+            }
           }
+        }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[0][i] += v[u][i];
-    }
+      px += n * sx;
+      if (YDT >= 0) py += n * sy;
+    };
+    int64_t k = 0;
+#pragma unroll 1
+    for (; k + U <= nr; k += U) step(U);
+    if (k < nr) step(static_cast<int>(nr - k));
   }
-#pragma unroll
-  for (int k = 0; k < NS; ++k)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) red[k][w][lane * 8 + i] = acc[k][i];
-  __syncthreads();
-  const int64_t c = blockIdx.x * 256LL + threadIdx.x;
+  const int64_t c = blockIdx.x * 256LL + threadIdx.x;  // threads < 256: one column each
   const int64_t nchunks = gridDim.y;
-  if (c < cols) {
+  // warps combine through shared memory in warp order into this chunk's partial
 #pragma unroll
-    for (int k = 0; k < NS; ++k) {
+  for (int k = 0; k < NS; ++k) {
+    if (k) __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[w][lane * 8 + i] = acc[k][i];
+    __syncthreads();
+    if (threadIdx.x < 256 && c < cols) {
       float t = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) t += red[k][q][threadIdx.x];
+#pragma unroll 8
+      for (int q = 0; q < kCsWarps; ++q) t += red[q][threadIdx.x];
       partial[(k * nchunks + blockIdx.y) * cols + c] = t;
     }
   }
@@ -229,19 +232,19 @@ __global__ void __launch_bounds__(256) colsum_chunk_kernel(const void* x, const 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // warp w sums chunks w, w + 8, ... (8 columns per lane, 4 chunks in flight), then the
-  // warps combine in order: a fixed association, so the result is deterministic
+  // warp w sums chunks w, w + kCsWarps, ... (8 columns per lane, 4 chunks in flight), then
+  // the warps combine in order: a fixed association, so the result is deterministic
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
     float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (c8 < cols) {
       const float* base = partial + k * nchunks * cols + c8;
 #pragma unroll 1
-      for (int64_t q0 = w; q0 < nchunks; q0 += 32) {
+      for (int64_t q0 = w; q0 < nchunks; q0 += 4 * kCsWarps) {
         float4 v[4][2];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int64_t q = q0 + 8 * u;
+          const int64_t q = q0 + kCsWarps * u;
           if (q < nchunks) {
             v[u][0] = __ldcg(reinterpret_cast<const float4*>(base + q * cols));
             v[u][1] = __ldcg(reinterpret_cast<const float4*>(base + q * cols + 4));
@@ -258,12 +261,12 @@ __global__ void __launch_bounds__(256) colsum_chunk_kernel(const void* x, const 
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 8; ++i) red[0][w][lane * 8 + i] = t[i];
+    for (int i = 0; i < 8; ++i) red[w][lane * 8 + i] = t[i];
     __syncthreads();
-    if (c < cols) {
+    if (threadIdx.x < 256 && c < cols) {
       float sum = 0.f;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) sum += red[0][q][threadIdx.x];
+#pragma unroll 8
+      for (int q = 0; q < kCsWarps; ++q) sum += red[q][threadIdx.x];
       (k == 0 ? out : out2)[c] = sum;
     }
   }
@@ -620,6 +623,145 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_kernel(const void* dy, int 
   }
 }
 
+// LayerNorm backward with its column sums (bf16 rows): dx as ln_bwd_vec_kernel, plus
+// dgamma = sum dy * xhat, dbeta = sum dy and, with RES, sum resid (the bias gradient of the
+// linear whose output gradient the residual carries) -- one read of every operand instead
+// of a separate column-sum pass. Persistent: a CTA's warps stride the rows, keep their
+// lanes' column sums in registers, combine them in warp order through shared memory and
+// write one partial row per CTA (partial[cta][k][cols]); colsum_parts_kernel sums those.
+template <int VPL, bool RES>
+__global__ void __launch_bounds__(256, 1) ln_bwd_sums_kernel(
+    const __nv_bfloat16* dy, const __nv_bfloat16* xhat, const float* gamma, const float* inv_std,
+    int64_t rows, const __nv_bfloat16* resid, __nv_bfloat16* dx, float* partial) {
+  constexpr int cols = 256 * VPL;
+  constexpr int NS = RES ? 3 : 2;
+  __shared__ float red[kWarpsPerBlock][cols];
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  auto lo = [](uint32_t u) { return __uint_as_float(u << 16); };
+  auto hi = [](uint32_t u) { return __uint_as_float(u & 0xffff0000u); };
+  float gm[VPL][8], acc[NS][VPL][8];
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) {
+    const int c = (k * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + c));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + c + 4));
+    gm[k][0] = g0.x; gm[k][1] = g0.y; gm[k][2] = g0.z; gm[k][3] = g0.w;
+    gm[k][4] = g1.x; gm[k][5] = g1.y; gm[k][6] = g1.z; gm[k][7] = g1.w;
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[j][k][i] = 0.f;
+  }
+  const float inv_h = 1.f / static_cast<float>(cols);
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + w; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * kWarpsPerBlock) {
+    uint4 qd[VPL], qx[VPL], qr[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const int64_t off = r * cols + (k * 32 + lane) * 8;
+      qd[k] = __ldg(reinterpret_cast<const uint4*>(dy + off));
+      qx[k] = __ldg(reinterpret_cast<const uint4*>(xhat + off));
+      if (RES) qr[k] = __ldg(reinterpret_cast<const uint4*>(resid + off));
+    }
+    const float inv = __ldg(inv_std + r);
+    float sg = 0.f, sd = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const uint32_t* ud = reinterpret_cast<const uint32_t*>(&qd[k]);
+      const uint32_t* ux = reinterpret_cast<const uint32_t*>(&qx[k]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = (i & 1) ? hi(ud[i / 2]) : lo(ud[i / 2]);
+        const float x = (i & 1) ? hi(ux[i / 2]) : lo(ux[i / 2]);
+        acc[0][k][i] = fmaf(d, x, acc[0][k][i]);
+        acc[1][k][i] += d;
+        const float g = d * gm[k][i];
+        sg += g;
+        sd = fmaf(g, x, sd);
+      }
+    }
+    sg = warp_sum(sg) * inv_h;
+    sd = warp_sum(sd) * inv_h;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      const uint32_t* ud = reinterpret_cast<const uint32_t*>(&qd[k]);
+      const uint32_t* ux = reinterpret_cast<const uint32_t*>(&qx[k]);
+      const uint32_t* ur = reinterpret_cast<const uint32_t*>(&qr[k]);
+      uint4 o;
+      uint32_t* uo = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        float v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float d = e ? hi(ud[i / 2]) : lo(ud[i / 2]);
+          const float x = e ? hi(ux[i / 2]) : lo(ux[i / 2]);
+          v[e] = inv * (d * gm[k][i + e] - sg - x * sd);
+          if (RES) {
+            const float rv = e ? hi(ur[i / 2]) : lo(ur[i / 2]);
+            acc[NS - 1][k][i + e] += rv;
+            v[e] += rv;
+          }
+        }
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[0], v[1]);
+        uo[i / 2] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      *reinterpret_cast<uint4*>(dx + r * cols + (k * 32 + lane) * 8) = o;
+    }
+  }
+  // warps combine in warp order; thread t owns columns t, t + 256, ...
+#pragma unroll
+  for (int j = 0; j < NS; ++j) {
+    if (j) __syncthreads();
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) red[w][(k * 32 + lane) * 8 + i] = acc[j][k][i];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int c = q * 256 + threadIdx.x;
+      float t = 0.f;
+#pragma unroll
+      for (int ww = 0; ww < kWarpsPerBlock; ++ww) t += red[ww][c];
+      partial[(static_cast<int64_t>(blockIdx.x) * NS + j) * cols + c] = t;
+    }
+  }
+}
+
+// out[j] for j < width: sum over parts p of partial[p][j], in part order (32 part groups
+// per column, then the groups in order: a fixed association). Block: 32 columns x 32 groups.
+__global__ void __launch_bounds__(1024) colsum_parts_kernel(const float* partial, int parts,
+                                                            int64_t width, int64_t seg,
+                                                            float* out0, float* out1, float* out2) {
+  __shared__ float red[32][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int64_t j = blockIdx.x * 32LL + tx;
+  float t = 0.f;
+  if (j < width) {
+    float v[8];
+    for (int p0 = ty; p0 < parts; p0 += 32 * 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int p = p0 + 32 * u;
+        v[u] = p < parts ? __ldcg(partial + static_cast<int64_t>(p) * width + j) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t += v[u];
+    }
+  }
+  red[ty][tx] = t;
+  __syncthreads();
+  if (ty == 0 && j < width) {
+    float sum = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < 32; ++q) sum += red[q][tx];
+    const int64_t k = j / seg;
+    float* o = k == 0 ? out0 : k == 1 ? out1 : out2;
+    o[j % seg] = sum;
+  }
+}
+
 __global__ void copy_heads_kernel(const void* src, int64_t src_ld, int64_t src_hs, void* dst,
                                   int64_t dst_ld, int64_t dst_hs, int64_t rows, int64_t heads,
                                   int64_t dh, int dt) {
@@ -674,8 +816,18 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
     return;
   }
   const bool dual = out_x && y;
-  const int64_t chunks = (rows + kCsRows - 1) / kCsRows;
   const int64_t tiles = (cols + 255) / 256;
+  // one wave of 1024-thread CTAs, one per SM, each summing a contiguous block of rows (a
+  // multiple of 32): no partial second wave, and few chunk partials for the finishing CTA
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    C3D_CUDA(cudaGetDevice(&dev));
+    C3D_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(num_sms / tiles, (rows + 31) / 32));
+  const int64_t rows_per_cta = ((rows + chunks - 1) / chunks + 31) / 32 * 32;
+  chunks = std::max<int64_t>(1, (rows + rows_per_cta - 1) / rows_per_cta);
   char* scratch = nullptr;
   const size_t pbytes = static_cast<size_t>((dual ? 2 : 1) * chunks * cols) * sizeof(float);
   C3D_CUDA(cudaMallocAsync(&scratch, pbytes + tiles * sizeof(unsigned), s));
@@ -685,7 +837,8 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
   dim3 g(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
   const int yk = y ? ydt : -1;
 #define C3D_COLSUM(XD, YD, DU) \
-  colsum_chunk_kernel<XD, YD, DU><<<g, 256, 0, s>>>(x, y, rows, cols, partial, counters, out, out_x)
+  colsum_chunk_kernel<XD, YD, DU><<<g, 32 * kCsWarps, 0, s>>>(x, y, rows, cols, rows_per_cta, partial, \
+                                                     counters, out, out_x)
   if (dual) {
     if (xdt == kBF16 && yk == kBF16) C3D_COLSUM(kBF16, kBF16, true);
     else if (xdt == kBF16) C3D_COLSUM(kBF16, kF32, true);
@@ -835,6 +988,57 @@ bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const flo
   else if (vpl == 4) launch(ln_bwd_vec_kernel<4>);
   else launch(ln_bwd_vec_kernel<8>);
   check_launch("ln_bwd_vec");
+  return true;
+}
+
+bool k_ln_bwd_sums(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                   const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
+                   void* dx, int dxdt, float* dgamma, float* dbeta, float* dresid,
+                   cudaStream_t s) {
+  const int vpl = ln_vpl(cols);
+  // the per-lane column sums live in registers: up to 1024 columns (VPL 4)
+  if (!vpl || vpl > 4 || dt != kBF16 || xdt != kBF16 || dxdt != kBF16 || (resid && rdt != kBF16) ||
+      (resid != nullptr) != (dresid != nullptr) || !al16(dy) || !al16(xhat) || !al16(gamma) || !al16(dx) ||
+      (resid && !al16(resid)))
+    return false;
+  if (rows == 0) {
+    C3D_CUDA(cudaMemsetAsync(dgamma, 0, cols * sizeof(float), s));
+    C3D_CUDA(cudaMemsetAsync(dbeta, 0, cols * sizeof(float), s));
+    if (dresid) C3D_CUDA(cudaMemsetAsync(dresid, 0, cols * sizeof(float), s));
+    return true;
+  }
+  static int num_sms = 0;
+  if (num_sms == 0) {
+    int dev = 0;
+    C3D_CUDA(cudaGetDevice(&dev));
+    C3D_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int ns = dresid ? 3 : 2;
+  const int grid = static_cast<int>(std::min<int64_t>(num_sms, (rows + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  float* partial = nullptr;
+  C3D_CUDA(cudaMallocAsync(&partial, static_cast<size_t>(grid) * ns * cols * sizeof(float), s));
+  const auto* d16 = static_cast<const __nv_bfloat16*>(dy);
+  const auto* x16 = static_cast<const __nv_bfloat16*>(xhat);
+  const auto* r16 = static_cast<const __nv_bfloat16*>(resid);
+  auto* o16 = static_cast<__nv_bfloat16*>(dx);
+  auto go = [&](auto V) {
+    constexpr int VV = decltype(V)::value;
+    if (dresid)
+      ln_bwd_sums_kernel<VV, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(d16, x16, gamma, inv_std,
+                                                                        rows, r16, o16, partial);
+    else
+      ln_bwd_sums_kernel<VV, false><<<grid, 32 * kWarpsPerBlock, 0, s>>>(d16, x16, gamma, inv_std,
+                                                                         rows, nullptr, o16, partial);
+  };
+  if (vpl == 1) go(std::integral_constant<int, 1>{});
+  else if (vpl == 2) go(std::integral_constant<int, 2>{});
+  else go(std::integral_constant<int, 4>{});
+  check_launch("ln_bwd_sums");
+  const int64_t width = static_cast<int64_t>(ns) * cols;
+  colsum_parts_kernel<<<static_cast<unsigned>((width + 31) / 32), 1024, 0, s>>>(
+      partial, grid, width, cols, dgamma, dbeta, dresid);
+  check_launch("colsum_parts");
+  C3D_CUDA(cudaFreeAsync(partial, s));
   return true;
 }
 

@@ -53,6 +53,13 @@ void k_combine_moments(const float* st, int P, int64_t rows, int64_t n, float* s
                        cudaStream_t s);
 // p_out = 1 backward in one pass (row sums and dx); false when the shape has no
 // vectorised form (the caller then runs k_ln_bwd_rows + k_ln_bwd_dx).
+// LayerNorm backward of bf16 rows with its column sums in the same pass: dgamma = sum
+// dy * xhat, dbeta = sum dy, and (resid given) dx += resid, dresid = sum resid. False (nothing
+// launched) when the shape / dtypes / alignment do not fit; resid and dresid go together.
+bool k_ln_bwd_sums(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
+                   const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
+                   void* dx, int dxdt, float* dgamma, float* dbeta, float* dresid,
+                   cudaStream_t s);
 bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
                     const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
                     void* dx, int dxdt, cudaStream_t s);

@@ -136,7 +136,9 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
     fail(C3D_ERR_DIRECTION_CLASH, "dC of C=AB backward must carry the swapped triple");
   // The reduction is collective: every rank joins it whether or not it holds a
   // diagonal slice (non-holders pass a vector with no local data).
-  if (sinks && sinks->bias_colsum) {
+  if (sinks && sinks->bias_elsewhere) {
+    // summed by the LayerNorm backward that reads dy as its residual (layer_bwd)
+  } else if (sinks && sinks->bias_colsum) {
     k_colsum(dyf.data, dyf.dtype, nullptr, kF32, dyf.rows, dyf.cols, sinks->bias_colsum, s);
   } else if (db) {
     DevBuf cs(static_cast<size_t>(dyf.cols) * sizeof(float), s);
@@ -211,12 +213,25 @@ void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, 
 }
 
 void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& sv, Act& dx, const Vec* dgamma,
-                   const Vec* dbeta, const void* resid, cudaStream_t s, float* sink) {
+                   const Vec* dbeta, const void* resid, cudaStream_t s, float* sink,
+                   float* resid_sink) {
   // layernorm3d_bwd (cube3d/nn.hpp:187-222)
   if (dy.group != sv.group || dy.hidden != sv.hidden)
     fail(C3D_ERR_SHAPE_MISMATCH, "layer norm gradient does not match the saved forward");
   const Dirs d = triple_for_group(dy.group);
   const float inv_h = 1.f / static_cast<float>(dy.hidden);
+  if (sink && cube.extent(d.out) == 1 && (resid_sink || !resid)) {
+    // one pass: dx, dgamma | dbeta into the sink and, with resid_sink, the residual's
+    // column sum (the bias gradient of the linear whose output gradient it is)
+    Act out = make_act(cube, dx.data, dx.dtype, dy.batch, dy.seq, dy.hidden, dy.group);
+    if (k_ln_bwd_sums(dy.data, dy.dtype, sv.xhat, sv.dtype, sv.gamma_block, sv.inv_std, dy.rows,
+                      dy.cols, resid_sink ? resid : nullptr, dx.dtype, out.data, out.dtype, sink,
+                      sink + dy.cols, resid_sink, s)) {
+      dx = out;
+      return;
+    }
+  }
+  if (resid_sink) k_colsum(resid, dy.dtype, nullptr, kF32, dy.rows, dy.cols, resid_sink, s);
   if (sink) {
     k_colsum(dy.data, dy.dtype, sv.xhat, sv.dtype, dy.rows, dy.cols, sink, s, sink + dy.cols);
   } else if (dgamma && dbeta) {  // collective on every rank (see linear_bwd)
@@ -749,6 +764,10 @@ void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const Lay
   const bool packed_vecs = !S.vec0.empty();
   if (!packed_vecs)
     for (auto& k : sk) k.bias_colsum = nullptr;  // each linear reduces its own bias grad
+  // b_fc2 = colsum(dy) and b_out = colsum(dy1): the two LayerNorm backwards read dy / dy1
+  // as their residuals and sum them in the same pass (with dgamma, dbeta)
+  const bool ln_sums = packed_vecs && dt == kBF16 && cube.extent(triple_for_group(grp).out) == 1;
+  if (ln_sums) sk[1].bias_elsewhere = sk[3].bias_elsewhere = true;
 
   DevBuf dn2b(bytes, s), dy1b(bytes, s), dn1b(bytes, s);
   Act dn2;
@@ -761,15 +780,16 @@ void layer_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const Lay
   dy1.data = dy1b.get();
   dy1.dtype = dt;
   layernorm_bwd(cube, dn2, S.ln2, dy1, &g.ln2_g, &g.ln2_b, dy.data, s,
-                packed_vecs ? f0 + 3 * c0 : nullptr);  // dy1 = dy + LN2'
+                packed_vecs ? f0 + 3 * c0 : nullptr,
+                ln_sums ? f0 + 5 * c0 : nullptr);  // dy1 = dy + LN2'
   Act dn1;
   dn1.data = dn1b.get();
   dn1.dtype = dt;
   attention_bwd(cube, mode, cfg, dy1, S.attn, p.qkv, p.out, dn1, g, s, wg[0], wg[1],
                 packed_vecs ? &sk[0] : (pack_dw ? &sk[0] : nullptr),
                 packed_vecs ? &sk[1] : (pack_dw ? &sk[1] : nullptr));
-  layernorm_bwd(cube, dn1, S.ln1, dx, &g.ln1_g, &g.ln1_b, dy1.data, s,
-                packed_vecs ? f0 : nullptr);  // dx = dy1 + LN1'
+  layernorm_bwd(cube, dn1, S.ln1, dx, &g.ln1_g, &g.ln1_b, dy1.data, s, packed_vecs ? f0 : nullptr,
+                ln_sums ? f0 + 2 * c0 : nullptr);  // dx = dy1 + LN1'
   if (packed_vecs) {
     Vec v0[6] = {g.ln1_g, g.ln1_b, g.b_out, g.ln2_g, g.ln2_b, g.b_fc2};
     for (auto& v : v0) v.len = cfg.hidden;

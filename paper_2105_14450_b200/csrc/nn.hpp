@@ -61,6 +61,7 @@ struct LinearPre {
 // un-reduced weight-gradient partial (reduced once per layer).
 struct LinearSinks {
   float* bias_colsum = nullptr;
+  bool bias_elsewhere = false;  // the bias gradient is summed by another pass (LN backward)
   DwSink dw;
 };
 struct LNSaved : Saved {
@@ -136,9 +137,12 @@ void linear_bwd(Cube& cube, int mode, const Act& dy, const LinearSaved& saved, c
 void layernorm_fwd(Cube& cube, const Act& x, const Vec& gamma, const Vec& beta, double eps,
                    Act& y, LNSaved* saved, cudaStream_t s, const float* gblock = nullptr,
                    const float* bblock = nullptr);
+// `colsum_sink`: dgamma | dbeta column sums land there (the caller reduces them);
+// `resid_sink`: also the residual's column sum (bias gradient of the linear whose output
+// gradient the residual is), from the same pass when the fused kernel applies.
 void layernorm_bwd(Cube& cube, const Act& dy, const LNSaved& saved, Act& dx, const Vec* dgamma,
                    const Vec* dbeta, const void* resid, cudaStream_t s,
-                   float* colsum_sink = nullptr);
+                   float* colsum_sink = nullptr, float* resid_sink = nullptr);
 
 void attention_fwd(Cube& cube, int mode, const Config& cfg, const Act& x, const LinearP& qkv,
                    const LinearP& out, int& group, Act& y, AttnSaved* saved, bool own_input,
