@@ -630,12 +630,12 @@ def our_arm(args, wl):
     sent_total = dist.sum_over_ranks(float(cnt["elements_sent"]))
     model_f, model_b = T.layer_traffic(b, s, n, h, cube.dims,
                                        flash=T.flash_applies(s, n, h, cube.dims, True))
-    traffic = {"elements_sent_all_ranks": sent_total, "model": model_f + model_b,
+    tparity = {"elements_sent_all_ranks": sent_total, "model": model_f + model_b,
                "match": sent_total == model_f + model_b}
     if cube.dims[0] == cube.dims[1] == cube.dims[2] and cube.dims[0] > 1:
         dev = T.reference_deviation(b, s, n, h, cube.dims[0])
-        traffic["reference_traffic_model"] = model_f + model_b + sum(dev.values())
-        traffic["below_reference_by"] = dev
+        tparity["reference_traffic_model"] = model_f + model_b + sum(dev.values())
+        tparity["below_reference_by"] = dev
     layer_tflops = layer_flops / (ms_max * 1e-3) / 1e12
     nvlink_gbs = 770.0  # measured peer bandwidth per direction (B200_PROFILING.md)
     bound = {"flop_ms": layer_flops / (peak_tc * 1e12 * world) * 1e3,
@@ -698,7 +698,7 @@ def our_arm(args, wl):
             "matmul": mm,
             "layer_frac_of_peak": layer_tflops / (peak_tc * world),
             "layer_roofline": layer_roofline,
-            "traffic_parity": traffic,
+            "traffic_parity": tparity,
             "fp32_mode": f32,
             "cfg4_training_step": cfg4,
             "collectives": {"calls_per_step": comm_n / prof_steps,

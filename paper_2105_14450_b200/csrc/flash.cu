@@ -430,8 +430,9 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
   uint64_t* dp_full = s_full + 1;
   uint64_t* p_full = dp_full + 1;
   uint64_t* ds_full = p_full + 1;
-  uint64_t* pds_free = ds_full + 1;
-  uint64_t* dq_full = pds_free + 1;        // 2 (per dQ buffer)
+  uint64_t* p_free = ds_full + 1;         // dV(it) done: the P buffer may be rewritten
+  uint64_t* ds_free = p_free + 1;         // dK(it), dQ(it) done: the dS buffer likewise
+  uint64_t* dq_full = ds_free + 1;        // 2 (per dQ buffer)
   uint64_t* dq_empty = dq_full + 2;       // 2
   uint64_t* acc_full = dq_empty + 2;
   uint64_t* acc_empty = acc_full + 1;
@@ -459,7 +460,8 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
     ptx::mbar_init(dp_full, 1);
     ptx::mbar_init(p_full, 32 * C::kEw);
     ptx::mbar_init(ds_full, 32 * C::kEw);
-    ptx::mbar_init(pds_free, 1);
+    ptx::mbar_init(p_free, 1);
+    ptx::mbar_init(ds_free, 1);
     for (int k = 0; k < 2; ++k) {
       ptx::mbar_init(dq_full + k, 1);
       ptx::mbar_init(dq_empty + k, 128);
@@ -563,6 +565,7 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
         if (i == 0 && j > 0) ptx::mbar_wait(acc_empty, (j - 1) & 1);  // dK, dV read out
         ptx::tc_fence_after();
         issue_acc(C::kColDV, sp, sdo, i > 0);
+        ptx::umma_commit(p_free);
         if (!C::kAlias && it + 1 < total) {
           ptx::mbar_wait(dp_cons, it & 1);
           issue_s(it + 1, true);
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
                          ptx::smem_desc_sw128(sk + 2048 * k, 128 * 128, 1024), kIdescDQ,
                          k > 0 ? 1u : 0u);
         ptx::umma_commit(dq_full + qb);
-        ptx::umma_commit(pds_free);
+        ptx::umma_commit(ds_free);
         ptx::umma_commit(q_empty + it % kQS);
         if (i == nq - 1) ptx::umma_commit(kv_empty + j % kKS);
         if (C::kAlias && it + 1 < total) {
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
                                                 fast_exp2(fmaf(v[4 * q4 + 3], c, -l4.w)));
         }
       }
-      if (it > 0) ptx::mbar_wait(pds_free, (it - 1) & 1);  // dV / dK / dQ of it-1 done
+      if (it > 0) ptx::mbar_wait(p_free, (it - 1) & 1);  // dV of it-1 done with P
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const int cg = cg0 + g;
@@ -642,6 +645,7 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
       ptx::mbar_arrive(p_full);
       ptx::mbar_wait(dp_full, it & 1);
       ptx::tc_fence_after();
+      if (it > 0) ptx::mbar_wait(ds_free, (it - 1) & 1);  // dK / dQ of it-1 done with dS
       {
         // dS^T = P^T (dP^T - D), unscaled: the softmax scale is applied to dK / dQ where
         // they leave TMEM (DH x fewer multiplies)

@@ -56,6 +56,14 @@ struct TcOperand {
 struct TcArgs {
   int M, N, K, batch;
   int cg;  // CTAs per tile (2: cta_group::2 pair, M = 256)
+  // k-segmented tiles (CTA pairs): each tile's K range is cut into sk segments, units
+  // run segment-major (the pairs of a wave share k windows in L2); the last segment of
+  // a tile to arrive (sk_count) finishes it, adding the others' fp32 partials (sk_ws,
+  // raised by sk_flag) in k order -- no separate reduction pass
+  int sk;               // segments per tile (0: off)
+  float* sk_ws;         // [tile][segment][rank][BN][128] (column-major partial tiles)
+  uint32_t* sk_flag;    // [tile][segment][rank]
+  uint32_t* sk_count;   // [tile][rank]
   int m_tiles, n_tiles, k_blocks;
   int group_m;  // tile rows per rasterisation band (1: plain m-major order)
   int num_tiles;  // output tiles (batch * m_tiles * n_tiles)
@@ -182,16 +190,17 @@ __device__ __forceinline__ void op_issue_pair(const CUtensorMap* map, const TcOp
 
 struct Unit {
   int b, m0, n0, kb0, kb1, ks;
+  int tile;   // tile index; sk_seg: -1 whole tile, else the k segment of a split tile
+  int sk_seg;
 };
 
 // CTA pairs (cg = 2): m tiles are 256-row pair tiles; CTA `rank` owns rows
 // [m0 + 128 rank, +128) of its pair's tile.
-__device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn, int rank = 0) {
+__device__ __forceinline__ Unit decode_tile(const TcArgs& a, int tile, int bn, int rank) {
   Unit u;
-  // split-major order: the persistent CTAs sweep K window by window together, so each
-  // window's operand footprint stays resident in L2 (no drift-induced thrash).
-  u.ks = t / a.num_tiles;
-  const int tile = t - u.ks * a.num_tiles;
+  u.ks = 0;
+  u.tile = tile;
+  u.sk_seg = -1;
   const int per_batch = a.m_tiles * a.n_tiles;
   u.b = tile / per_batch;
   const int rem = tile - u.b * per_batch;
@@ -206,11 +215,44 @@ __device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn, int 
   const int mt = first_m + (within - nt * gsize);
   u.m0 = mt * kBM * a.cg + rank * kBM;
   u.n0 = nt * bn;
-  u.kb0 = u.ks * a.kb_per_split;
+  u.kb0 = 0;
+  u.kb1 = a.k_blocks;
+  return u;
+}
+
+__device__ __forceinline__ Unit decode_unit(const TcArgs& a, int t, int bn, int rank = 0) {
+  // split-major order: the persistent CTAs sweep K window by window together, so each
+  // window's operand footprint stays resident in L2 (no drift-induced thrash).
+  const int ks = t / a.num_tiles;
+  Unit u = decode_tile(a, t - ks * a.num_tiles, bn, rank);
+  u.ks = ks;
+  u.kb0 = ks * a.kb_per_split;
   u.kb1 = min(a.k_blocks, u.kb0 + a.kb_per_split);
   return u;
 }
 
+// The units of CTA (pair) `id` of `stride`, round-robin: tiles, split-K windows, or
+// (tile, k segment) pairs in segment-major order.
+struct UnitIter {
+  int t, stride;
+  __device__ __forceinline__ UnitIter(const TcArgs&, int id, int stride_) : t(id), stride(stride_) {}
+  __device__ __forceinline__ bool next(const TcArgs& a, int bn, int rank, Unit& u) {
+    if (!a.sk) {
+      if (t >= a.num_tiles * a.ksplit) return false;
+      u = decode_unit(a, t, bn, rank);
+      t += stride;
+      return true;
+    }
+    if (t >= a.num_tiles * a.sk) return false;
+    const int seg = t / a.num_tiles;
+    u = decode_tile(a, t - seg * a.num_tiles, bn, rank);
+    u.kb0 = seg * a.k_blocks / a.sk;
+    u.kb1 = (seg + 1) * a.k_blocks / a.sk;
+    u.sk_seg = seg;
+    t += stride;
+    return true;
+  }
+};
 __device__ __forceinline__ void load8(const void* base, int dtype, long long off, float* out) {
   if (dtype == kF32) {
     const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(base) + off);
@@ -459,6 +501,51 @@ __device__ __forceinline__ void epi_math32(const TcArgs& args, long long off, in
   }
 }
 
+// Stream-K fix-up of a finishing segment: the other segments' fp32 partial rows (this
+// lane's row, the warp's column base) in k order; `self` is this segment's position.
+struct SkFix {
+  int n = -1;                   // segments - 1
+  int self = 0;                 // this segment's position
+  const float* base = nullptr;  // the tile's segment 0 partial (+ rank / lane / column offset)
+  size_t seg_stride = 0;        // elements between consecutive segments' partials
+  __device__ __forceinline__ const float* part(const TcArgs&, int q) const {
+    return base + static_cast<size_t>(q) * seg_stride;
+  }
+};
+
+// Replaces this warp's accumulator columns in TMEM by the sum of all segments of the
+// split tile, in k order (this segment's accumulator at its position): the regular
+// epilogue then runs unchanged.
+template <int COLS>
+__device__ __forceinline__ void sk_fixup(const TcArgs& a, const SkFix& fx, uint32_t row_taddr) {
+#pragma unroll 1
+  for (int c = 0; c < COLS / 32; ++c) {
+    float v[32];
+    ptx::tmem_ld32(row_taddr + 32 * c, v);
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += 8) {
+      float t8[8];
+#pragma unroll 1
+      for (int q = 0; q <= fx.n; ++q) {
+        float pv[8];
+        if (q == fx.self) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pv[i] = v[j0 + i];
+        } else {
+          const float* src = fx.part(a, q) + (32 * c + j0) * kBM;  // column-major partial
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pv[i] = __ldcg(src + i * kBM);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t8[i] = q == 0 ? pv[i] : t8[i] + pv[i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[j0 + i] = t8[i];
+    }
+    ptx::tmem_st32(row_taddr + 32 * c, v);
+  }
+}
+
 template <int CW, int COLS>
 __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorMap* tmC,
                                              const CUtensorMap* tmX, uint8_t* buf, uint8_t* xbuf,
@@ -597,6 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* x_bar = tempty_bar + 2;  // one per epilogue warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_bar + kEpiWarps);
+  uint32_t* sk_last = tmem_slot + 1;  // stream-K: this CTA finishes the current split tile
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -633,8 +721,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       OpPos pa, pb;
       const uint32_t full_leader = CG == 2 ? ptx::mapa(ptx::smem_u32(full_bar), 0) : 0u;
-      for (int t = cta_id; t < units; t += cta_stride) {
-        const Unit u = decode_unit(args, t, BN, rank);
+      UnitIter ui(args, cta_id, cta_stride);
+      Unit u;
+      while (ui.next(args, BN, rank, u)) {
         op_init(args.a, pa, u.m0, A_MN ? kBM / 64 : 1, u.kb0 * kBK, u.b);
         op_init(args.b, pb, u.n0 + rank * kBRows, B_MN ? kBRows / 64 : 1, u.kb0 * kBK, u.b);
         for (int kb = u.kb0; kb < u.kb1; ++kb) {
@@ -668,8 +757,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t aph = 0;
       const uint32_t a0 = ptx::smem_u32(smem_a), b0 = ptx::smem_u32(smem_b);
-      for (int t = cta_id; t < units; t += cta_stride) {
-        const Unit u = decode_unit(args, t, BN);
+      UnitIter ui(args, cta_id, cta_stride);
+      Unit u;
+      while (ui.next(args, BN, 0, u)) {
         ptx::mbar_wait(&tempty_bar[acc], aph ^ 1);
         ptx::tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
@@ -719,8 +809,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                  e.pre_act != nullptr);
       const uint32_t epoch = args.rs_P ? *args.rs_epoch : 0u;
       uint32_t entered_mask = 0;
-      for (int t = cta_id; t < units; t += cta_stride) {
-        const Unit u = decode_unit(args, t, BN, rank);
+      UnitIter ui(args, cta_id, cta_stride);
+      Unit u;
+      while (ui.next(args, BN, rank, u)) {
         const int mrow0 = u.m0 + quarter * 32;
         const int m = mrow0 + lane;
         const bool row_ok = m < args.M;
@@ -747,13 +838,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t row_taddr = tmem_base + acc * BN +
                                    (static_cast<uint32_t>(quarter * 32) << 16) + half * kColsPerWarp;
         const int ncol0 = u.n0 + half * kColsPerWarp;
-        if (args.cw == 32)
-          epi_tile_tma<32, kColsPerWarp>(args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr,
-                                         ncol0, row_off, row_ok, c1, c2r, c3, c4);
-        else
-          epi_tile_tma<(kColsPerWarp >= 64 ? 64 : 32), kColsPerWarp>(
-              args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr, ncol0, row_off, row_ok, c1,
-              c2r, c3, c4);
+        SkFix fx;
+        bool finish = true;
+        if (u.sk_seg >= 0) {
+          // a k segment of a split tile: the last of its segments to arrive finishes it
+          // partials are column-major per CTA tile ([BN][128]): for each column a warp's 32
+          // rows are 128 contiguous bytes, so every store / load is one coalesced line
+          const size_t lane_off = static_cast<size_t>(half * kColsPerWarp) * kBM + quarter * 32 + lane;
+          const size_t slot_elems = static_cast<size_t>(kBM) * BN;
+          const int S = args.sk;
+          if (threadIdx.x == 64) {
+            const uint32_t prev = atomicAdd(&args.sk_count[u.tile * 2 + rank], 1u);
+            *sk_last = prev + 1 == static_cast<uint32_t>(S) ? 1u : 0u;
+          }
+          ptx::named_bar(1, 32 * kEpiWarps);
+          finish = *sk_last != 0;
+          ptx::named_bar(1, 32 * kEpiWarps);
+          const size_t slot0 = static_cast<size_t>(u.tile) * S;
+          if (!finish) {
+            // raw fp32 partial into the segment's slot, then raise its flag
+            float* w = args.sk_ws + ((slot0 + u.sk_seg) * 2 + rank) * slot_elems + lane_off;
+#pragma unroll 1
+            for (int c = 0; c < kColsPerWarp / 32; ++c) {
+              float v[32];
+              ptx::tmem_ld32(row_taddr + 32 * c, v);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) __stcg(w + (32 * c + j) * kBM, v[j]);
+            }
+            __threadfence();
+            ptx::named_bar(1, 32 * kEpiWarps);
+            if (threadIdx.x == 64)
+              ptx::st_release_gpu(&args.sk_flag[(slot0 + u.sk_seg) * 2 + rank], 1u);
+          } else {
+            // the other segments' partials (their flags: they have arrived, may still be
+            // writing), summed with this one in k order
+            if (lane == 0)
+              for (int q = 0; q < S; ++q) {
+                if (q == u.sk_seg) continue;
+                while (ptx::ld_acquire_gpu(&args.sk_flag[(slot0 + q) * 2 + rank]) == 0) {
+                }
+              }
+            __syncwarp();
+            fx.n = S - 1;
+            fx.self = u.sk_seg;
+            fx.base = args.sk_ws + (slot0 * 2 + rank) * slot_elems + lane_off;
+            fx.seg_stride = 2 * slot_elems;
+            sk_fixup<kColsPerWarp>(args, fx, row_taddr);
+          }
+        }
+        if (finish) {
+          if (args.cw == 32)
+            epi_tile_tma<32, kColsPerWarp>(args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr,
+                                           ncol0, row_off, row_ok, c1, c2r, c3, c4);
+          else
+            epi_tile_tma<(kColsPerWarp >= 64 ? 64 : 32), kColsPerWarp>(
+                args, cmap, &tmP, buf, xbuf, xbar, xph, lane, row_taddr, ncol0, row_off, row_ok, c1,
+                c2r, c3, c4);
+        }
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -775,7 +916,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else
-    for (int t = cta_id; t < units; t += cta_stride) {
+    for (int t = cta_id; t < units; t += cta_stride) {  // (no stream-K without TMA stores)
       const Unit u = decode_unit(args, t, BN, rank);
       const int m = u.m0 + quarter * 32 + lane;
       // row offset once per unit (the only divisions on the epilogue path)
@@ -1018,8 +1159,22 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     if (std::getenv("C3D_GEMM_VERBOSE"))
       std::fprintf(stderr, "tc_gemm pair kernel: %d resident pairs\n", max_pairs);
   }
-  cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_pairs)));
+  char* skbuf = nullptr;
+  if (args.sk) {
+    const size_t ws = static_cast<size_t>(args.num_tiles) * args.sk * 2 * kBM * BN * sizeof(float);
+    const size_t flags = static_cast<size_t>(args.num_tiles) * args.sk * 2 * sizeof(uint32_t);
+    const size_t counts = static_cast<size_t>(args.num_tiles) * 2 * sizeof(uint32_t);
+    C3D_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&skbuf), ws + flags + counts, stream));
+    C3D_CUDA(cudaMemsetAsync(skbuf + ws, 0, flags + counts, stream));
+    args.sk_ws = reinterpret_cast<float*>(skbuf);
+    args.sk_flag = reinterpret_cast<uint32_t*>(skbuf + ws);
+    args.sk_count = reinterpret_cast<uint32_t*>(skbuf + ws + flags);
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(args.num_tiles * args.sk, max_pairs)));
+  } else {
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_pairs)));
+  }
   C3D_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mp, args, rsm));
+  if (skbuf) C3D_CUDA(cudaFreeAsync(skbuf, stream));
 }
 
 template <int BN>
@@ -1027,12 +1182,14 @@ void launch_bn(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
                const CUtensorMap& mp, TcArgs& args, const RsMaps& rsm, int num_sms,
                cudaStream_t stream) {
   const bool am = args.a.mn_major, bm = args.b.mn_major;
-  if (BN == 256 && args.cg == 2) {
+  if constexpr (BN == 256) {
+    if (args.cg == 2) {
     if (!am && !bm) launch_tc<BN, false, false, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
     else if (!am && bm) launch_tc<BN, false, true, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
     else if (am && !bm) launch_tc<BN, true, false, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
     else launch_tc<BN, true, true, 2>(ma, mb, mc, mp, args, rsm, num_sms, stream);
     return;
+    }
   }
   if (!am && !bm) launch_tc<BN, false, false>(ma, mb, mc, mp, args, rsm, num_sms, stream);
   else if (!am && bm) launch_tc<BN, false, true>(ma, mb, mc, mp, args, rsm, num_sms, stream);
@@ -1169,9 +1326,36 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   // bands of 16 tile rows once the B operand outgrows a comfortable share of L2
   args.group_m = (p.N * p.K * 2 > (48ll << 20)) ? std::min(16, args.m_tiles) : 1;
   if (const char* e = std::getenv("C3D_GROUP_M")) args.group_m = std::max(1, std::min(std::atoi(e), args.m_tiles));
-  args.ksplit = p.rs.P > 1 ? 1
-                            : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms,
-                                          bn);
+  // stream-K on CTA pairs when 256 x 256 pair tiles leave a poor last wave and K is long
+  // (the weight-gradient products: 48 tiles of 1024 x 3072 x 16384 on 74 pairs)
+  int sk = 0;
+  if (bn == 256 && p.rs.P <= 1 && p.batch == 1 && !p.epi.pre_act && args.m_tiles >= 2 &&
+      !std::getenv("C3D_NO_SK") && !std::getenv("C3D_NO_CG2")) {
+    // segments per tile: the best wave fill, each extra segment charged 3% (its fp32
+    // partial round trip), and only for a clear gain. Measured on B200: a segment must keep
+    // >= 64 k-blocks of main loop, or its partial / fix-up epilogue outweighs the better
+    // wave fill (1024 x 3072 x 16384 in 3 segments: 99.8 us vs 102.8; 16384 x 1024 x 4096
+    // in 2: 137.6 vs 104.9); tile counts that suit single-CTA split-K keep that path
+    // (1024 x 1024 x 16384: 53.7 us split-K vs 60.9 in 4 segments)
+    const int pairs = num_sms / 2;
+    const int ptiles = static_cast<int>((p.M + 2 * kBM - 1) / (2 * kBM)) * args.n_tiles;
+    auto eff = [&](int S) {
+      const int units = ptiles * S;
+      const int waves = (units + pairs - 1) / pairs;
+      return static_cast<double>(units) / (static_cast<double>(waves) * pairs) - 0.03 * (S - 1);
+    };
+    double best = eff(1);
+    const bool splitk = pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch, num_sms, bn) > 1;
+    for (int S = 2; S <= 8 && args.k_blocks / S >= 64 && !splitk; ++S)
+      if (eff(S) > best + 0.15) {
+        best = eff(S);
+        sk = S;
+      }
+    if (const char* e = std::getenv("C3D_SK")) sk = std::max(0, std::atoi(e));  // experiments
+  }
+  args.ksplit = (p.rs.P > 1 || sk) ? 1
+                                    : pick_ksplit(p.M, p.N, args.num_tiles, args.k_blocks, p.batch,
+                                                  num_sms, bn);
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
   args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
   // CTA pairs (cta_group::2, 256 x 256 tiles) for plain 256-wide tiles
@@ -1181,6 +1365,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     args.m_tiles = static_cast<int>((p.M + 2 * kBM - 1) / (2 * kBM));
     args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
     args.group_m = std::min(args.group_m, args.m_tiles);
+    args.sk = sk > 1 ? sk : 0;
   }
   args.epi = p.epi;
   // vector loads/stores need 16-B aligned rows and 32-column chunks
@@ -1266,6 +1451,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     sv = View();
   }
   args.tma_store = tma ? 1 : 0;
+  if (!tma) args.sk = 0;  // the split-tile fix-up lives in the TMA-store epilogue
   args.st_rsplit = static_cast<int>(sv.rsplit);
   args.st_csplit = static_cast<int>(sv.csplit);
   args.st_blo = sv.b_lo_n;

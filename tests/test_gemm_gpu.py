@@ -127,3 +127,31 @@ def test_grouped_rasterisation_large_b(torch_cuda, a_mn, b_mn):
     got, ref = _run(torch, 128 * 20, 4096, 8192, a_mn, b_mn, integer=True)
     assert not torch.isnan(got).any()
     assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("shape,a_mn,b_mn,segs", [((1024, 3072, 16384), True, True, None),
+                                                  ((1024, 1024, 16384), True, True, "4"),
+                                                  ((4096, 1024, 8192), True, False, "3"),
+                                                  ((16384, 1024, 1024), False, True, "2")])
+def test_k_segmented_exact(torch_cuda, monkeypatch, shape, a_mn, b_mn, segs):
+    """Pair tiles that leave a poor last wave are cut into k segments (the 1024 x 3072 x
+    16384 weight gradient takes 3 by itself; C3D_SK forces a count): the last segment of a
+    tile to arrive adds the others' fp32 partials. Integer inputs keep every partial sum
+    exact, so the result is bitwise the fp32 product."""
+    torch = torch_cuda
+    if segs:
+        monkeypatch.setenv("C3D_SK", segs)
+    M, N, K = shape
+    got, ref = _run(torch, M, N, K, a_mn, b_mn, integer=True)
+    assert not torch.isnan(got).any()
+    assert torch.equal(got, ref)
+
+
+def test_k_segmented_deterministic(torch_cuda):
+    """The split tiles' partials are summed in k order whichever segment finishes last:
+    two runs on real-valued inputs agree bitwise, and match fp32 to rounding."""
+    torch = torch_cuda
+    a, ref = _run(torch, 1024, 3072, 16384, True, True)
+    b, _ = _run(torch, 1024, 3072, 16384, True, True)
+    assert torch.equal(a, b)
+    assert (a - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
