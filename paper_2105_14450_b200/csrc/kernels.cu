@@ -45,6 +45,13 @@ __global__ void apply_epilogue_kernel(const void* in, int in_dt, int64_t rows, i
   }
 }
 
+__global__ void convert_batch_kernel(ConvBatch b) {
+  const ConvSeg& g = b.seg[blockIdx.y];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < g.n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    st_any(g.dst, g.ddt, i, ld_any(g.src, g.sdt, i));
+}
+
 __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int64_t n) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -856,6 +863,22 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
   check_launch("colsum_chunk");
   if (out_x && !y) C3D_CUDA(cudaMemcpyAsync(out_x, out, cols * sizeof(float), cudaMemcpyDeviceToDevice, s));
   C3D_CUDA(cudaFreeAsync(scratch, s));
+}
+
+void k_convert_batch(const ConvSeg* segs, int n, cudaStream_t s) {
+  for (int i0 = 0; i0 < n; i0 += ConvBatch::kMax) {
+    ConvBatch b;
+    const int m = std::min(n - i0, ConvBatch::kMax);
+    int64_t most = 0;
+    for (int i = 0; i < m; ++i) {
+      b.seg[i] = segs[i0 + i];
+      most = std::max(most, segs[i0 + i].n);
+    }
+    if (most == 0) continue;
+    const unsigned bx = static_cast<unsigned>(std::min<int64_t>((most + 255) / 256, 148 * 4));
+    convert_batch_kernel<<<dim3(bx, static_cast<unsigned>(m)), 256, 0, s>>>(b);
+    check_launch("convert_batch");
+  }
 }
 
 void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s) {

@@ -24,6 +24,18 @@ void k_colsum(const void* x, int xdt, const void* y, int ydt, int64_t rows, int6
               float* out, cudaStream_t s, float* out_x = nullptr);
 
 void k_convert(const void* src, int sdt, void* dst, int ddt, int64_t n, cudaStream_t s);
+// Several conversions in one launch (grid.y = segment).
+struct ConvSeg {
+  const void* src;
+  void* dst;
+  int sdt, ddt;
+  int64_t n;
+};
+struct ConvBatch {
+  static constexpr int kMax = 8;
+  ConvSeg seg[kMax];
+};
+void k_convert_batch(const ConvSeg* segs, int n, cudaStream_t s);
 // y = gelu(x), x <- gelu'(x) (n elements, in place on x).
 void k_gelu_save(void* x, int xdt, void* y, int ydt, int64_t n, cudaStream_t s);
 

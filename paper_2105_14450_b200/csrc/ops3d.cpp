@@ -270,8 +270,10 @@ void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
       fail(C3D_ERR_LENGTH_MISMATCH, "diagonal rank holds no buffer for its vector slice");
   }
   if (g.size() == 1) {
+    std::vector<ConvSeg> cv;
     for (size_t k = 0; k < outs.size(); ++k)
-      k_convert(colsums + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
+      cv.push_back(ConvSeg{colsums + off[k], outs[k].data, kF32, outs[k].dtype, n2[k]});
+    k_convert_batch(cv.data(), static_cast<int>(cv.size()), s);
     return;
   }
   // column-sum blocks [k][u][q slice] -> position-major [u][q][k slice]; reduce-scatter
@@ -296,9 +298,12 @@ void reduce_to_diagonal_multi(Cube& cube, const Dirs& d, const float* colsums,
     C3D_CUDA(cudaMemcpyAsync(slice.get(), cur, S * sizeof(float), cudaMemcpyDeviceToDevice, s));
   }
   if (pl.cube_rule() && pl.Pi > 1) cube.all_reduce(d.in, slice.get(), S, kF32, false, s);
-  if (holder)
+  if (holder) {
+    std::vector<ConvSeg> cv;
     for (size_t k = 0; k < outs.size(); ++k)
-      k_convert(slice.as<float>() + off[k], kF32, outs[k].data, outs[k].dtype, n2[k], s);
+      cv.push_back(ConvSeg{slice.as<float>() + off[k], outs[k].data, kF32, outs[k].dtype, n2[k]});
+    k_convert_batch(cv.data(), static_cast<int>(cv.size()), s);
+  }
 }
 
 void add_vec_fwd(Cube& cube, const Mat& a, const Vec& b, Mat& c, cudaStream_t s) {
