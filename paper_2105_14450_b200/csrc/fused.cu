@@ -280,6 +280,9 @@ bool gemm_reduce_scatter(Cube& cube, int mode, int axis, int64_t M, int64_t N, i
   if (!h || P < 2 || P > kRsMax || mode == C3D_MODE_F32) return false;
   if (a.dtype != kBF16 || b.dtype != kBF16 || M % P) return false;
   if (std::getenv("C3D_NO_FUSED_RS")) return false;
+  // the finishing pass addresses the output (and residual / aux / pre-activation, which
+  // share its layout) as contiguous [rows][N] blocks
+  if (post.out.sr != N || post.out.sc != 1 || post.out.csplit || post.out.rsplit) return false;
   const int dtype = post.out.dtype;
   const long long es = dtype == kF32 ? 4 : 2;
   const long long block_rows = M / P;
