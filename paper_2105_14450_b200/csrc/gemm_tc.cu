@@ -1170,6 +1170,10 @@ void launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& 
     args.sk_flag = reinterpret_cast<uint32_t*>(skbuf + ws);
     args.sk_count = reinterpret_cast<uint32_t*>(skbuf + ws + flags);
     cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(args.num_tiles * args.sk, max_pairs)));
+  } else if (args.rs_P) {
+    // fused reduce-scatter: the grid must be the one tc_gemm_grid reported (done flags);
+    // its CTAs wait only on other GPUs, never on each other, so co-residency is not needed
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, num_sms / 2)));
   } else {
     cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min(units, max_pairs)));
   }
@@ -1297,7 +1301,19 @@ bool tc_gemm_rs_supported(const GemmProblem& p, int bn) {
   return true;
 }
 
+// CTA pairs for 256-wide tiles (the decision tc_gemm_launch takes for unsplit products).
+static bool use_pairs(const GemmProblem& p, int bn, int ksplit) {
+  // with a fused reduce-scatter every CTA's 128 rows must fall inside the blocks
+  return bn == 256 && ksplit == 1 && !std::getenv("C3D_NO_CG2") && (p.M + kBM - 1) / kBM >= 2 &&
+         (p.rs.P <= 1 || p.M % (2 * kBM) == 0);
+}
+
 int tc_gemm_grid(const GemmProblem& p, int bn, int num_sms) {
+  // the fused reduce-scatter (ksplit 1) sizes its done flags by this grid
+  if (use_pairs(p, bn, 1)) {
+    const long long ptiles = ((p.M + 2 * kBM - 1) / (2 * kBM)) * ((p.N + bn - 1) / bn) * p.batch;
+    return static_cast<int>(2 * std::min<long long>(ptiles, num_sms / 2));
+  }
   const long long tiles = ((p.M + kBM - 1) / kBM) * ((p.N + bn - 1) / bn) * p.batch;
   return static_cast<int>(std::min<long long>(tiles, num_sms));
 }
@@ -1359,8 +1375,7 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
   args.kb_per_split = (args.k_blocks + args.ksplit - 1) / args.ksplit;
   args.ksplit = (args.k_blocks + args.kb_per_split - 1) / args.kb_per_split;
   // CTA pairs (cta_group::2, 256 x 256 tiles) for plain 256-wide tiles
-  if (bn == 256 && args.ksplit == 1 && p.rs.P <= 1 && !std::getenv("C3D_NO_CG2") &&
-      args.m_tiles >= 2) {
+  if (use_pairs(p, bn, args.ksplit)) {
     args.cg = 2;
     args.m_tiles = static_cast<int>((p.M + 2 * kBM - 1) / (2 * kBM));
     args.num_tiles = args.m_tiles * args.n_tiles * p.batch;
