@@ -111,6 +111,11 @@ struct FwdCfg {
   static constexpr int kSmem = 1024 + kOffBar + 256;
   static constexpr int kColO = 2 * BK;  // S0 [0,BK), S1 [BK,2BK), O0, O1 after
   static constexpr int kThreads = 64 + 256;
+  // TMEM columns (a power of two): with <= 256 two CTAs share an SM, so one CTA's
+  // prologue (Q load, first S) and epilogue (O readout) overlap the other's key loop
+  static constexpr int kTmemNeed = 2 * BK + 2 * DH;
+  static constexpr int kTmemCols = kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512);
+  static constexpr int kMinBlocks = (kTmemCols <= 256 && kSmem <= 112 * 1024) ? 2 : 1;
 };
 
 struct FwdArgs {
@@ -122,7 +127,7 @@ struct FwdArgs {
 };
 
 template <int DH, int BK>
-__global__ void __launch_bounds__(FwdCfg<DH, BK>::kThreads, 1)
+__global__ void __launch_bounds__(FwdCfg<DH, BK>::kThreads, FwdCfg<DH, BK>::kMinBlocks)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const FwdArgs args) {
   using C = FwdCfg<DH, BK>;
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, BK>::kThreads, 1)
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, BK>::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<512>(tmem);
+    ptx::tmem_dealloc<C::kTmemCols>(tmem);
   }
 }
 
@@ -807,7 +812,10 @@ bool flash_fwd(const View& q, const View& k, const View& v, const View& ctx, flo
   }
   if (k.rsplit || v.rsplit || (q.rsplit && q.rsplit % 128) || !out_ok(ctx, static_cast<int>(H)))
     return false;
-  const int bk = dh == 64 ? 128 : 64;
+  // dh 64: key blocks of 64 (256 TMEM columns, two CTAs per SM); C3D_FWD_BK128 keeps
+  // the one-CTA-per-SM variant with key blocks of 128
+  static const bool bk128 = std::getenv("C3D_FWD_BK128") != nullptr;
+  const int bk = dh == 64 && bk128 ? 128 : 64;
   int mn = 0;
   const CUtensorMap mq = tc_operand_map(q, S, dh, nslices, 128, &mn);
   if (mn) return false;
@@ -823,7 +831,8 @@ bool flash_fwd(const View& q, const View& k, const View& v, const View& ctx, flo
   a.q_split = static_cast<int>(q.rsplit);
   a.ctx = out_view(ctx);
   a.lse = lse;
-  if (dh == 64) launch_fwd<64, 128>(mq, mk, mv, a, nslices, s);
+  if (dh == 64 && bk == 128) launch_fwd<64, 128>(mq, mk, mv, a, nslices, s);
+  else if (dh == 64) launch_fwd<64, 64>(mq, mk, mv, a, nslices, s);
   else launch_fwd<128, 64>(mq, mk, mv, a, nslices, s);
   check_launch("flash_fwd");
   return true;
