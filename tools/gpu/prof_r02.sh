@@ -14,7 +14,7 @@ timeout 900 ncu --set full --clock-control none -k regex:tc_gemm -s 12 -c 12 -o 
 ncu -i gpurun_out/${TAG}_gemm.ncu-rep --page raw --csv > gpurun_out/${TAG}_gemm_raw.csv 2>/dev/null
 rm -f gpurun_out/${TAG}_gemm.ncu-rep
 timeout 900 ncu --set full --clock-control none -k "regex:flash|ln_bwd_sums|ln_fwd|colsum|rowdot|convert|splitk" \
-    -s 20 -c 20 -o gpurun_out/${TAG}_other python tools/profile_step.py 1 > gpurun_out/${TAG}_other_ncu.log 2>&1; echo "other ncu rc=$?"
+    -s 14 -c 14 -o gpurun_out/${TAG}_other python tools/profile_step.py 1 > gpurun_out/${TAG}_other_ncu.log 2>&1; echo "other ncu rc=$?"
 ncu -i gpurun_out/${TAG}_other.ncu-rep --page raw --csv > gpurun_out/${TAG}_other_raw.csv 2>/dev/null
 rm -f gpurun_out/${TAG}_other.ncu-rep
 ls -la gpurun_out/ | grep $TAG
