@@ -597,9 +597,13 @@ __device__ __forceinline__ void epi_tile_tma(const TcArgs& args, const CUtensorM
         }
         if (e.act == kActGeluSave) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float x = v[j];
-            gelu_both(x, v[j], pre[j]);
+          for (int j = 0; j < 32; j += 2) {
+            float2 g2, d2;
+            gelu_both2(make_float2(v[j], v[j + 1]), g2, d2);
+            v[j] = g2.x;
+            v[j + 1] = g2.y;
+            pre[j] = d2.x;
+            pre[j + 1] = d2.y;
           }
         } else {
 #pragma unroll

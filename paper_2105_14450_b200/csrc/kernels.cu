@@ -82,7 +82,14 @@ __global__ void gelu_save_kernel(void* x, int xdt, void* y, int ydt, int64_t n, 
         v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) gelu_both(v[i], g[i], d[i]);
+      for (int i = 0; i < 8; i += 2) {
+        float2 g2, d2;
+        gelu_both2(make_float2(v[i], v[i + 1]), g2, d2);
+        g[i] = g2.x;
+        g[i + 1] = g2.y;
+        d[i] = d2.x;
+        d[i + 1] = d2.y;
+      }
       auto put = [&](void* base, int dt, const float* w) {
         if (dt == kBF16) {
           uint4 q;
