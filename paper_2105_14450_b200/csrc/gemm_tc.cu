@@ -985,6 +985,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Split-K reduction, plain epilogue into a contiguous output: 4 columns per thread, all
+// splits' loads in flight (the weight-gradient case).
+__global__ void splitk_reduce4_kernel(const float* ws, int ksplit, long long total4, void* out,
+                                      int out_dtype) {
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total4;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 acc = __ldcs(reinterpret_cast<const float4*>(ws) + t);
+    for (int k = 1; k < ksplit; ++k) {
+      const float4 x = __ldcs(reinterpret_cast<const float4*>(ws) + k * total4 + t);
+      acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+    }
+    if (out_dtype == kF32) {
+      reinterpret_cast<float4*>(out)[t] = acc;
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&lo);
+      u.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[t] = u;
+    }
+  }
+}
+
 // Split-K reduction: out = epilogue(sum_k ws[k][m][n]) in ascending split order.
 __global__ void splitk_reduce_kernel(const float* ws, int ksplit, int M, int N, Epilogue e) {
   const long long total = static_cast<long long>(M) * N;
@@ -1484,7 +1507,20 @@ void tc_gemm_launch(const GemmProblem& p, int bn, int num_sms, cudaStream_t stre
     check_launch("tc_gemm(split-k)");
     const long long total = p.M * p.N;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
-    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, args.ksplit, args.M, args.N, p.epi);
+    const Epilogue& e = p.epi;
+    const bool plain = !e.bias && e.act == kActNone && !e.pre_act && !e.aux && !e.resid &&
+                       !e.accumulate && e.alpha == 1.f && !e.rowvec;
+    const bool contig = e.out.sr == p.N && e.out.sc == 1 && !e.out.rsplit && !e.out.csplit &&
+                        p.batch == 1 && p.N % 4 == 0 &&
+                        reinterpret_cast<uintptr_t>(e.out.base) % 16 == 0;
+    if (plain && contig) {
+      const long long total4 = total / 4;
+      const int b4 = static_cast<int>(std::min<long long>((total4 + 255) / 256, 148LL * 8));
+      splitk_reduce4_kernel<<<b4, 256, 0, stream>>>(ws, args.ksplit, total4, e.out.base,
+                                                    e.out.dtype);
+    } else {
+      splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(ws, args.ksplit, args.M, args.N, p.epi);
+    }
     C3D_CUDA(cudaFreeAsync(ws, stream));
   }
 }

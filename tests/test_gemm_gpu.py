@@ -131,6 +131,7 @@ def test_grouped_rasterisation_large_b(torch_cuda, a_mn, b_mn):
 
 @pytest.mark.parametrize("shape,a_mn,b_mn,segs", [((1024, 3072, 16384), True, True, None),
                                                   ((1024, 1024, 16384), True, True, "4"),
+                                                  ((1024, 1024, 16384), True, True, "0"),
                                                   ((4096, 1024, 8192), True, False, "3"),
                                                   ((16384, 1024, 1024), False, True, "2")])
 def test_k_segmented_exact(torch_cuda, monkeypatch, shape, a_mn, b_mn, segs):
@@ -155,3 +156,11 @@ def test_k_segmented_deterministic(torch_cuda):
     b, _ = _run(torch, 1024, 3072, 16384, True, True)
     assert torch.equal(a, b)
     assert (a - ref).abs().max().item() <= 1e-3 * max(1.0, ref.abs().max().item())
+
+
+def test_split_k_bf16_output(torch_cuda, monkeypatch):
+    """Few tiles, long K: single-CTA split-K whose vectorised reduction writes bf16."""
+    torch = torch_cuda
+    monkeypatch.setenv("C3D_SK", "0")
+    got, ref = _run(torch, 1024, 1024, 16384, True, True, out_dtype=torch.bfloat16)
+    assert ((got - ref).abs() <= 1e-2 * ref.abs().clamp(min=1)).all()
