@@ -409,6 +409,9 @@ struct BwdArgs {
   long long rd_split;
   OutView dq, dk, dv;
   float* dq_ws;                     // [slice][S/128][DH][128] fp32 scratch
+  // head dim 64, unsplit outputs: column sums of the stored dQ / dK / dV (the QKV bias
+  // gradient), per (batch, drain warp): [batch][4][H][3 * 64], q | k | v per head
+  float* bias_part;
 };
 
 template <int DH>
@@ -714,6 +717,21 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
             make_uint4(pack_bf16x2(v[8 * p + 0], v[8 * p + 1]), pack_bf16x2(v[8 * p + 2], v[8 * p + 3]),
                        pack_bf16x2(v[8 * p + 4], v[8 * p + 5]), pack_bf16x2(v[8 * p + 6], v[8 * p + 7]));
     };
+    // QKV bias gradient (head dim 64): column sums of every staged bf16 tile over this
+    // warp's 32 rows -- lane L owns columns 2L, 2L + 1 (one pair per row, conflict-free)
+    float bs[3][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};  // q, k, v
+    auto sum_staged = [&](float (&acc)[2]) {
+      __syncwarp();
+#pragma unroll 8
+      for (int rr = 0; rr < 32; ++rr) {
+        const int R = quarter * 32 + rr;
+        const uint32_t u = *reinterpret_cast<const uint32_t*>(
+            stg + R * 128 + (((lane >> 2) ^ (R & 7)) << 4) + (lane & 3) * 4);
+        acc[0] += __uint_as_float(u << 16);
+        acc[1] += __uint_as_float(u & 0xffff0000u);
+      }
+    };
+    const bool want_bias = DH == 64 && args.bias_part != nullptr;
     for (int it = 0; it < total; ++it) {
       const int j = it / nq, i = it % nq;
       if (i == nq - 1) {
@@ -737,6 +755,7 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
             ptx::tc_fence_before();
             ptx::mbar_arrive(acc_empty);
           }
+          if (want_bias) sum_staged(bs[which == 0 ? 2 : 1]);
           stage_store(which == 0 ? &tmDV : &tmDK, 64 * ch, j * 128, 0);
         }
       }
@@ -769,8 +788,19 @@ __global__ void __launch_bounds__(BwdCfg<DH>::kThreads, 1)
             stage_row(v, half);
           }
         }
-        if (last) stage_store(&tmDQ, 64 * ch, i * 128, args.q_split_dq);
+        if (last) {
+          if (want_bias) sum_staged(bs[0]);
+          stage_store(&tmDQ, 64 * ch, i * 128, args.q_split_dq);
+        }
       }
+    }
+    if (want_bias) {
+      // [batch][drain warp][head][q | k | v][64]
+      float* p = args.bias_part +
+                 ((static_cast<long long>(c4) * 4 + quarter) * args.H + c3) * (3 * 64) + 2 * lane;
+#pragma unroll
+      for (int part = 0; part < 3; ++part)
+        *reinterpret_cast<float2*>(p + 64 * part) = make_float2(bs[part][0], bs[part][1]);
     }
   }
   ptx::tc_fence_before();
@@ -849,8 +879,9 @@ size_t flash_bwd_workspace_bytes(int64_t S, int64_t dh, int nslices) {
 bool flash_bwd(const View& q, const View& k, const View& v, const View& d_o, const float* lse,
                const float* rowdot, int64_t rd_split, const View& dq, const View& dk, const View& dv,
                void* ws, int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
-               cudaStream_t s) {
+               cudaStream_t s, float* bias_part) {
   if (!flash_supported(S, keys, dh) || H <= 0 || !lse || !rowdot || !ws) return false;
+  if (bias_part && (dh != 64 || q.rsplit || dq.rsplit)) return false;
   for (const View* w : {&q, &k, &v, &d_o}) {
     if (w->dtype != kBF16 || reinterpret_cast<uintptr_t>(w->base) % 16) return false;
     if (w->csplit || w->b_lo_n != H || w->sc != 1) return false;
@@ -887,6 +918,7 @@ bool flash_bwd(const View& q, const View& k, const View& v, const View& d_o, con
   a.dk = out_view(dk);
   a.dv = out_view(dv);
   a.dq_ws = static_cast<float*>(ws);
+  a.bias_part = bias_part;
   CUtensorMap mdq, mdk, mdv;
   if (!tc_store_map(dq, S, dh, nslices, 64, 128, &mdq) ||
       !tc_store_map(dk, keys, dh, nslices, 64, 128, &mdk) ||

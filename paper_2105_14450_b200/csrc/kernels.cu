@@ -1021,6 +1021,13 @@ bool k_ln_bwd_fused(const void* dy, int dt, const void* xhat, int xdt, const flo
   return true;
 }
 
+void k_colsum_parts(const float* partial, int parts, int64_t width, float* out, cudaStream_t s) {
+  if (width == 0) return;
+  colsum_parts_kernel<<<static_cast<unsigned>((width + 31) / 32), 1024, 0, s>>>(
+      partial, parts, width, width, out, nullptr, nullptr);
+  check_launch("colsum_parts");
+}
+
 bool k_ln_bwd_sums(const void* dy, int dt, const void* xhat, int xdt, const float* gamma,
                    const float* inv_std, int64_t rows, int64_t cols, const void* resid, int rdt,
                    void* dx, int dxdt, float* dgamma, float* dbeta, float* dresid,

@@ -36,6 +36,8 @@ struct ConvBatch {
   ConvSeg seg[kMax];
 };
 void k_convert_batch(const ConvSeg* segs, int n, cudaStream_t s);
+// out[j] = sum over p < parts of partial[p][j] (j < width), in part order.
+void k_colsum_parts(const float* partial, int parts, int64_t width, float* out, cudaStream_t s);
 // y = gelu(x), x <- gelu'(x) (n elements, in place on x).
 void k_gelu_save(void* x, int xdt, void* y, int ydt, int64_t n, cudaStream_t s);
 

@@ -502,11 +502,24 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
       dqv = packed_out(dq_partial.get(), dt, a, true);
     }
     const View qv = a.Ps > 1 ? packed_view(S.q_full, dt, a, false) : qkv_view(qkv, dt, a, 0, false);
+    // b_qkv = colsum(dQKV): summed by the kernel's drain warps from the tiles they store
+    // (head dim 64, unsplit query rows), per (batch, warp) partials finished here
+    const bool fuse_bq = a.Ps == 1 && a.dh == 64 && qkv_sinks && qkv_sinks->bias_colsum &&
+                         !qkv_sinks->bias_elsewhere;
+    DevBuf bq;
+    if (fuse_bq) bq = DevBuf(static_cast<size_t>(a.bl * 4 * a.H * 3 * a.dh) * sizeof(float), s);
     if (!flash_bwd(qv, qkv_view(qkv, dt, a, 1, false), qkv_view(qkv, dt, a, 2, false),
                    packed_view(dcf.ptr, dt, a, false), S.lse, rd.as<float>(), rd_split, dqv,
                    qkv_view(dqkv_buf.get(), dt, a, 1, false), qkv_view(dqkv_buf.get(), dt, a, 2, false),
-                   ws, a.S, a.sl, a.dh, a.H, nslices, a.scale, s))
+                   ws, a.S, a.sl, a.dh, a.H, nslices, a.scale, s, fuse_bq ? bq.as<float>() : nullptr))
       fail(C3D_ERR_INTERNAL, "flash attention backward rejected the forward's layout");
+    LinearSinks qs;
+    if (qkv_sinks) qs = *qkv_sinks;
+    if (fuse_bq) {
+      k_colsum_parts(bq.as<float>(), static_cast<int>(a.bl * 4), a.H * 3 * a.dh,
+                     qkv_sinks->bias_colsum, s);
+      qs.bias_elsewhere = true;
+    }
     cube.add_madds(4ull * static_cast<uint64_t>(nslices) * a.S * a.sl * a.dh);
     if (a.Ps > 1) {
       DevBuf dq(static_cast<size_t>(rows * a.hd) * dtype_size(dt), s);
@@ -515,7 +528,7 @@ void attention_bwd(Cube& cube, int mode, const Config& cfg, const Act& dy, const
     }
     Act dqkv = make_act(cube, dqkv_buf.get(), dt, dy.batch, dy.seq, 3 * cfg.hidden, dctx.group);
     linear_bwd(cube, mode, dqkv, S.qkv_lin, qkv_p, &dx, &g.w_qkv, &g.b_qkv, nullptr, s, qkv_wg,
-               qkv_sinks);
+               qkv_sinks ? &qs : nullptr);
     return;
   }
   // unfused path: dP = dctx_full V^T (fp32)

@@ -39,7 +39,7 @@ size_t flash_bwd_workspace_bytes(int64_t S, int64_t dh, int nslices);
 bool flash_bwd(const View& q, const View& k, const View& v, const View& d_o, const float* lse,
                const float* rowdot, int64_t rd_split, const View& dq, const View& dk, const View& dv,
                void* ws, int64_t S, int64_t keys, int64_t dh, int64_t H, int nslices, float scale,
-               cudaStream_t s);
+               cudaStream_t s, float* bias_part = nullptr);
 
 // One (batched) local GEMM on this rank, charging batch*M*N*K multiply-adds.
 void gemm_views(Cube& cube, int mode, int64_t M, int64_t N, int64_t K, int batch, const View& a,
